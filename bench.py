@@ -1,0 +1,357 @@
+"""bench.py — headline benchmark (BASELINE.json metric) for crvec-b200.
+
+Metric: "CR Gelem/s per function at 2^28 fp32 (% HBM roofline); 2^32 sweep s @1-8 GPU".
+
+Workload at N=1 (BASELINE.json configs[1]): the log family — logf, log2f,
+log10f, log1pf — each over 2^28 binary32 inputs including denormals / Inf /
+NaN (tests/inputs.py:log_family_input), RNE. One step = one pass of the four
+kernels over their 2^28 inputs (4 * 2^28 elements, 8 GiB of HBM traffic).
+Inputs are 1 GiB per function (> 126 MB L2), so no L2 flush is needed.
+
+  value      device-resident throughput (Gelem/s, all ranks), CUDA events on
+             the launch stream, barrier + synchronize around the K timed steps,
+             max over ranks.
+  e2e        same metric through the C ABI host-pointer entry points
+             (crvec_logf ... with pinned host buffers): every step includes the
+             H2D copy of the inputs and the D2H copy of the results.
+  roofline   the dominant kernel (logf's k_map_vec): 8 algorithmic bytes per
+             element x 2^28 / its average event-timed duration vs the measured
+             HBM copy bandwidth of MEASURED_PEAKS.json.
+  cpu_baseline  the reference's own CPU path (ziv_correctly_round_f32 of the
+             reference oracle compiled by `make -C oracle ref`, FuncId::log) on
+             a bounded sample of the same inputs, all host threads, rank 0.
+  sweep      exhaustive 2^32 x 4-mode sweep of all 19 functions, sharded by
+             chunk range across ranks, one NCCL all_reduce of the per-chunk
+             hashes; seconds (max over ranks) and mismatching chunks vs golden.
+
+--impl reference times the reference CPU path alone (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CR Gelem/s per function at 2^28 fp32 (% HBM roofline); 2^32 sweep s @1-8 GPU"
+LOG_FAMILY = ["logf", "log2f", "log10f", "log1pf"]
+N_ELEM = 1 << 28
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ reference arm --
+def cpu_reference(fn_oracle: str, sample: int, threads: int = 0):
+    """Time the reference's own CPU path (ziv_correctly_round_f32, RNE)."""
+    from oracle import oracle as O
+    from tests.inputs import log_family_input
+    x = log_family_input("logf", sample, seed=3)
+    use_ref = O.ref_available() and fn_oracle in O.REF_FNS
+    t0 = time.perf_counter()
+    if use_ref:
+        O.ref_f32(fn_oracle, x, 0, threads)
+    else:
+        O.f32(fn_oracle, x, 0, threads, use_ld=False)
+    dt = time.perf_counter() - t0
+    return sample / dt / 1e9, ("reference" if use_ref else "port"), dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sample = args.cpu_sample
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference("log", sample)
+    for _ in range(args.steps):
+        v, kind, _ = cpu_reference("log", sample)
+        vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gelem/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sample / (value * 1e9) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "logf (FuncId::log) over the config-2 log-family input distribution, RNE",
+                   "sample_elems_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "Gelem/s", "cores": cores, "kind": kind,
+                         "sample": f"{sample} elements of the 2^28 config-2 logf input per step"},
+        "e2e": {"value": value, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ sweep ----
+def run_sweep(rank, world, fns):
+    """Exhaustive 2^32 sweep of `fns`, chunks sharded across ranks, one
+    all_reduce of the per-chunk hashes (NCCL); returns (seconds, mismatches)."""
+    import torch
+    import paper_2605_15547_b200 as crvec
+    per = 4096 // world
+    lo, hi = rank * per, (rank + 1) * per
+    names = list(fns)
+    hashes = torch.zeros((len(names) + 1, 4096, 4), dtype=torch.int64, device="cuda")
+    ctr = torch.zeros(4, dtype=torch.int64, device="cuda")
+    L = crvec.lib()
+    stream = torch.cuda.current_stream()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i, name in enumerate(names):
+        h = hashes[i, lo:hi]
+        h2 = hashes[len(names), lo:hi] if name == "sincosf" else None
+        rc = L.crvec_sweep_f32(crvec.FN_IDS[name], lo, hi, h.data_ptr(),
+                               h2.data_ptr() if h2 is not None else None, ctr.data_ptr(), 0,
+                               __import__("ctypes").c_void_p(stream.cuda_stream))
+        assert rc == 0, rc
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(hashes)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    secs = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
+    mism = 0
+    checked = 0
+    hh = hashes.cpu().numpy().view(np.uint64)
+    for i, name in enumerate(names):
+        if name == "sincosf":
+            pairs = [("sin", hh[i]), ("cos", hh[len(names)])]
+        else:
+            pairs = [(crvec.ORACLE_NAME[name], hh[i])]
+        for g, arr in pairs:
+            p = os.path.join(ROOT, "tests", "golden", "sweep", g + ".npy")
+            if os.path.exists(p):
+                mism += int((np.load(p) != arr).any(1).sum())
+                checked += 1
+    return secs, mism, checked, int(ctr[0].item())
+
+
+# --------------------------------------------------------------- our arm -----
+def run_crvec(args, rank, world, local):
+    import ctypes
+    import torch
+    import paper_2605_15547_b200 as crvec
+    from tests.inputs import log_family_input
+
+    L = crvec.lib()
+    n = N_ELEM
+    fns = LOG_FAMILY
+    # synthetic inputs generated on host, resident in HBM before timing
+    xs = {f: torch.from_numpy(log_family_input(f, n, seed=3 + i).view(np.float32)).cuda()
+          for i, f in enumerate(fns)}
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step(evs=None):
+        for i, f in enumerate(fns):
+            if evs is not None:
+                evs[f][0].record(stream)
+            rc = L.crvec_eval_f32_dev(crvec.FN_IDS[f], xs[f].data_ptr(), y.data_ptr(), None, n, 0, sp)
+            if evs is not None:
+                evs[f][1].record(stream)
+            assert rc == 0, rc
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    per_fn = {f: [] for f in fns}
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            evs = {f: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for f in fns}
+            step(evs)
+            per_fn_events = evs
+            for f in fns:
+                per_fn[f].append(per_fn_events[f])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    secs = max_over_ranks(t0.elapsed_time(t1) / 1e3, world)
+    elems_step = n * len(fns) * world
+    value = elems_step * args.steps / secs / 1e9
+    fn_ms = {f: float(np.mean([a.elapsed_time(b) for a, b in per_fn[f]])) for f in fns}
+    peak, peak_kind = peaks()
+    dom = max(fns, key=lambda f: fn_ms[f])
+    achieved = 8.0 * n / (fn_ms[dom] / 1e3) / 1e9
+    per_fn_gelem = {f: n / (fn_ms[f] / 1e3) / 1e9 for f in fns}
+
+    # ---- e2e: C ABI host-pointer path, pinned host buffers, copies in region
+    hx = {f: torch.from_numpy(log_family_input(f, n, seed=3 + i).view(np.float32)).pin_memory()
+          for i, f in enumerate(fns)}
+    hy = torch.empty(n, dtype=torch.float32).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+
+    def e2e_step():
+        for f in fns:
+            rc = L.crvec_eval_f32(crvec.FN_IDS[f], hx[f].data_ptr(), hy.data_ptr(), None, n, 0)
+            assert rc == 0, rc
+
+    e2e_step()
+    barrier(world)
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_secs = max_over_ranks(time.perf_counter() - t, world)
+    e2e_value = elems_step * e2e_steps / e2e_secs / 1e9
+
+    # ---- exhaustive sweep (sharded across ranks)
+    sweep = None
+    if not args.no_sweep:
+        secs_sw, mism, checked, nacc = run_sweep(rank, world, crvec.F32_FUNCS + ["sincosf"])
+        sweep = {"seconds": secs_sw, "functions": 19, "modes": 4, "patterns": 2 ** 32,
+                 "mismatching_chunks": mism, "golden_sets_checked": checked,
+                 "accurate_path_lanes": nacc, "ranks": world,
+                 "collective": "one NCCL all_reduce of 20x4096x4 u64 chunk hashes" if world > 1 else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, kind, dt = cpu_reference("log", args.cpu_sample)
+        cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": kind,
+               "sample": f"{args.cpu_sample} elements of the config-2 logf input (RNE), {dt:.1f} s"}
+
+    launches = len(fns) * args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "log family (logf, log2f, log10f, log1pf) x 2^28 fp32 each, "
+                                   "config-2 inputs incl. denormals/Inf/NaN, RNE, HBM-resident",
+                       "elements_per_step_per_gpu": n * len(fns), "l2": "inputs 1 GiB > L2, no flush",
+                       "per_function_gelem_s": per_fn_gelem, "per_function_ms": fn_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"k_map_vec<{dom}> (8 B/elem x 2^28)", "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "Gelem/s",
+                    "h2d_bytes_per_step": 4 * n * len(fns), "d2h_bytes_per_step": 4 * n * len(fns)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="crvec", choices=["crvec", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=1 << 21)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    rank, world, local = dist_init()
+    run_crvec(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

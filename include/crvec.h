@@ -1,0 +1,150 @@
+/* crvec.h — C ABI of the B200-native correctly rounded (CR) vector math library.
+ *
+ * Drop-in array boundary for the paper's CR functions (arxiv 2605.15547,
+ * "Correctly Rounded Functions For Vector Applications"). The reference's
+ * public surface is C++ templates over lane batches; each entry point below
+ * replaces one of them with an array-in/array-out call:
+ *
+ *   crvec_exp2f / crvec_exp2f_dev  <- template cr_exp2f<W>(Batch<float,W>, RoundingMode, Backend)
+ *                                     and cr_exp2f_scalar(float, RoundingMode)
+ *                                     (ref: proj/include/crvec/kernels_f32.hpp:27-35,
+ *                                      proj/src/kernels_f32.cpp:170-181)
+ *   crvec_log2f / crvec_log2f_dev  <- cr_log2f<W>, cr_log2f_scalar
+ *                                     (ref: proj/include/crvec/kernels_f32.hpp:30-35,
+ *                                      proj/src/kernels_f32.cpp:171,183-191)
+ *   crvec_<fn>f for the other 17 binary32 functions of ref: PAPER.md:49
+ *                                     (no reference code; same contract)
+ *   crvec_exp2 / crvec_log (+ _dev) <- cr_exp2<W>, cr_log<W>, cr_exp2_scalar, cr_log_scalar,
+ *                                     cr_exp2_counted / cr_log_counted with FastPathStats
+ *                                     (ref: proj/include/crvec/kernels_f64.hpp:58-81)
+ *   crvec_sweep_f32                <- exhaustive_f32 of the verify module
+ *                                     (ref: SPEC.md:250-258; proj/src/verify.cpp:1 is a stub)
+ *
+ * Conventions (ref: proj/include/crvec/fpbits.hpp:13-18, SPEC.md "[OP] cr_exp2f"):
+ *   - rounding modes are numbered as the reference's RoundingMode;
+ *   - every bit pattern is accepted; specials are values, never errors:
+ *     NaN in -> quiet(x) (payload and sign kept), invalid -> +qNaN 0x7FC00000;
+ *   - return 0 on success or a negative CRVEC_E* code; no exceptions cross
+ *     the ABI; there is no CPU fallback: without a usable CUDA device every
+ *     entry point returns CRVEC_ENODEV;
+ *   - host-pointer calls are synchronous; _dev calls take device pointers
+ *     and a cudaStream_t (passed as void*, NULL = default stream) and are
+ *     stream-ordered; in-place (x == y) is allowed; any alignment accepted.
+ *   - reentrant: the library keeps only a mutex-guarded staging workspace for
+ *     the host-pointer calls and device-side counters.
+ */
+#ifndef CRVEC_H
+#define CRVEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CRVEC_RNE = 0, /* RoundingMode::NearestEven */
+  CRVEC_RZ = 1,  /* RoundingMode::TowardZero */
+  CRVEC_RU = 2,  /* RoundingMode::TowardPositive */
+  CRVEC_RD = 3   /* RoundingMode::TowardNegative */
+} crvec_mode_t;
+
+/* Function ids; the first three follow the reference FuncId order
+ * (ref: proj/include/crvec/oracle.hpp:21). */
+typedef enum {
+  CRVEC_FN_EXP2F = 0, CRVEC_FN_LOGF = 1, CRVEC_FN_LOG2F = 2, CRVEC_FN_EXPF = 3,
+  CRVEC_FN_EXP10F = 4, CRVEC_FN_EXPM1F = 5, CRVEC_FN_LOG10F = 6, CRVEC_FN_LOG1PF = 7,
+  CRVEC_FN_SINF = 8, CRVEC_FN_COSF = 9, CRVEC_FN_TANF = 10, CRVEC_FN_ASINF = 11,
+  CRVEC_FN_ACOSF = 12, CRVEC_FN_ATANF = 13, CRVEC_FN_SINHF = 14, CRVEC_FN_COSHF = 15,
+  CRVEC_FN_TANHF = 16, CRVEC_FN_RSQRTF = 17, CRVEC_FN_SINCOSF = 18,
+  CRVEC_FN_COUNT = 19
+} crvec_fn_t;
+
+#define CRVEC_OK 0
+#define CRVEC_EINVAL (-1)  /* bad mode / function id / null pointer with n > 0 */
+#define CRVEC_ECUDA (-2)   /* CUDA runtime error (see crvec_last_cuda_error) */
+#define CRVEC_ENOMEM (-3)  /* device allocation failed */
+#define CRVEC_ENODEV (-4)  /* no usable sm_100 device */
+
+/* Fast-path accounting, mirrors FastPathStats (ref: proj/include/crvec/kernels_f64.hpp:72-81)
+ * extended with the accurate-path tiers of this implementation. */
+typedef struct {
+  uint64_t lanes;              /* elements evaluated */
+  uint64_t fast_undecided;     /* lanes whose fast-path rounding test failed */
+  uint64_t accurate_undecided; /* fp64: lanes whose accurate-path test also failed */
+  uint64_t host_callouts;      /* fp64: lanes resolved by the counted last resort */
+} crvec_stats_t;
+
+/* ---- binary32, host pointers (synchronous) ---- */
+int crvec_expf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_exp2f(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_exp10f(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_expm1f(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_logf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_log2f(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_log10f(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_log1pf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_sinf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_cosf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_tanf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_asinf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_acosf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_atanf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_sinhf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_coshf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_tanhf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_rsqrtf(const float *x, float *y, size_t n, crvec_mode_t mode);
+int crvec_sincosf(const float *x, float *s, float *c, size_t n, crvec_mode_t mode);
+
+/* ---- binary32, device pointers (stream-ordered) ---- */
+int crvec_expf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_exp2f_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_exp10f_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_expm1f_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_logf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_log2f_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_log10f_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_log1pf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_sinf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_cosf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_tanf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_asinf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_acosf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_atanf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_sinhf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_coshf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_tanhf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_rsqrtf_dev(const float *x, float *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_sincosf_dev(const float *x, float *s, float *c, size_t n, crvec_mode_t mode, void *stream);
+
+/* Generic forms (y2 used by CRVEC_FN_SINCOSF only). */
+int crvec_eval_f32(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n, crvec_mode_t mode);
+int crvec_eval_f32_dev(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n,
+                       crvec_mode_t mode, void *stream);
+
+/* ---- exhaustive binary32 sweep (verify) ----
+ * For chunks [chunk_lo, chunk_hi) of 2^20 bit patterns (chunk c = patterns
+ * c<<20 .. (c<<20)+2^20-1), adds into hashes[(c - chunk_lo)*4 + mode]
+ *   sum_p mix64(((uint64)out_mode(p) << 32) | p)   (mod 2^64)
+ * for all four modes at once; for CRVEC_FN_SINCOSF, hashes2 receives the cos
+ * outputs' hashes. hashes / hashes2 / counters are DEVICE pointers and must be
+ * zeroed by the caller (the sweep accumulates). counters[0] += fast-path
+ * lanes sent to the accurate path. force_accurate != 0 routes every non-
+ * special lane through the accurate path (self-check of that path). */
+int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *hashes,
+                    uint64_t *hashes2, uint64_t *counters, int force_accurate, void *stream);
+
+/* ---- accounting / errors ---- */
+int crvec_stats_get(crvec_stats_t *out);   /* cumulative since load / last reset */
+int crvec_stats_reset(void);
+const char *crvec_strerror(int code);
+const char *crvec_last_cuda_error(void);
+const char *crvec_version(void);
+int crvec_fn_count(void);
+const char *crvec_fn_name(crvec_fn_t fn);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRVEC_H */

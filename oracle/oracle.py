@@ -1,0 +1,185 @@
+"""ctypes bindings for the CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Importable only from tests/, ``__graft_entry__.smoke()`` and bench.py's CPU
+baseline / reference arm (the checker, never the thing measured or shipped).
+
+Two libraries:
+  * ``oracle/libcrvec_oracle.so`` — the C restatement of the reference oracle
+    (ref: proj/src/oracle.cpp) extended to the 18 MPFR functions;
+  * ``oracle/_ref/libcrvec_ref.so`` — the reference's OWN oracle compiled from
+    /root/reference/proj/src/{fpbits,oracle}.cpp (``make -C oracle ref``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcrvec_oracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libcrvec_ref.so")
+
+# Oracle function ids (first three = reference FuncId order,
+# ref: proj/include/crvec/oracle.hpp:21).
+FN = {
+    "exp2": 0, "log": 1, "log2": 2, "exp": 3, "exp10": 4, "expm1": 5,
+    "log10": 6, "log1p": 7, "sin": 8, "cos": 9, "tan": 10, "asin": 11,
+    "acos": 12, "atan": 13, "sinh": 14, "cosh": 15, "tanh": 16, "rsqrt": 17,
+}
+REF_FNS = ("exp2", "log", "log2")
+MODES = ("rne", "rz", "ru", "rd")
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_lib = None
+_ref = None
+
+
+def build(ref: bool = True) -> None:
+    """Compile the oracle (and the reference oracle when /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE, "libcrvec_oracle.so"], check=True)
+    if ref and os.path.isdir("/root/reference/proj"):
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build(ref=False)
+        L = ctypes.CDLL(LIB_PATH)
+        L.crvec_oracle_f32.restype = ctypes.c_uint32
+        L.crvec_oracle_f32.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.crvec_oracle_f64.restype = ctypes.c_uint64
+        L.crvec_oracle_f64.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int)]
+        L.crvec_oracle_f32_all_modes.argtypes = [ctypes.c_int, ctypes.c_uint32, _u32p, ctypes.c_int]
+        L.crvec_oracle_f64_all_modes.argtypes = [ctypes.c_int, ctypes.c_uint64, _u64p]
+        L.crvec_oracle_f32_batch.argtypes = [ctypes.c_int, _u32p, _u32p, ctypes.c_uint64,
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.crvec_oracle_f64_batch.argtypes = [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64,
+                                             ctypes.c_int, ctypes.c_int]
+        L.crvec_oracle_sweep_hashes.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                                _u64p, ctypes.c_int, ctypes.c_int]
+        L.crvec_oracle_convert_f64_to_f32.restype = ctypes.c_uint32
+        L.crvec_oracle_convert_f64_to_f32.argtypes = [ctypes.c_uint64, ctypes.c_int]
+        for name in ("cap_failures", "cap_input", "mpfr_calls", "ld_decided"):
+            getattr(L, "crvec_oracle_" + name).restype = ctypes.c_uint64
+        L.crvec_oracle_mix64.restype = ctypes.c_uint64
+        L.crvec_oracle_mix64.argtypes = [ctypes.c_uint64]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        R = ctypes.CDLL(REF_PATH)
+        R.crvec_ref_ziv_f32.restype = ctypes.c_uint32
+        R.crvec_ref_ziv_f32.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int)]
+        R.crvec_ref_ziv_f64.restype = ctypes.c_uint64
+        R.crvec_ref_ziv_f64.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int)]
+        R.crvec_ref_all_modes_f32.argtypes = [ctypes.c_int, ctypes.c_uint32, _u32p]
+        R.crvec_ref_all_modes_f64.argtypes = [ctypes.c_int, ctypes.c_uint64, _u64p]
+        R.crvec_ref_convert_f64_to_f32.restype = ctypes.c_uint32
+        R.crvec_ref_convert_f64_to_f32.argtypes = [ctypes.c_uint64, ctypes.c_int]
+        R.crvec_ref_batch_f32.argtypes = [ctypes.c_int, _u32p, _u32p, ctypes.c_uint64, ctypes.c_int,
+                                          ctypes.c_int]
+        R.crvec_ref_batch_f64.argtypes = [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.c_int,
+                                          ctypes.c_int]
+        _ref = R
+    return _ref
+
+
+def _p32(a):
+    return a.ctypes.data_as(_u32p)
+
+
+def _p64(a):
+    return a.ctypes.data_as(_u64p)
+
+
+def f32(fn: str, xbits: np.ndarray, mode: int | None = None, threads: int = 0,
+        use_ld: bool = True) -> np.ndarray:
+    """Correctly rounded binary32 results (as uint32 bit patterns).
+
+    mode None -> array of shape (n, 4) indexed by RoundingMode."""
+    x = np.ascontiguousarray(xbits, dtype=np.uint32)
+    n = x.size
+    if mode is None:
+        y = np.empty((n, 4), dtype=np.uint32)
+        m = -1
+    else:
+        y = np.empty(n, dtype=np.uint32)
+        m = int(mode)
+    before = lib().crvec_oracle_cap_failures()
+    rc = lib().crvec_oracle_f32_batch(FN[fn], _p32(x), _p32(y), n, m, threads, int(use_ld))
+    if rc != 0 or lib().crvec_oracle_cap_failures() != before:
+        raise RuntimeError(f"oracle: {fn} undecidable at precision cap "
+                           f"(input 0x{lib().crvec_oracle_cap_input():08x})")
+    return y
+
+
+def f64(fn: str, xbits: np.ndarray, mode: int | None = None, threads: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(xbits, dtype=np.uint64)
+    n = x.size
+    if mode is None:
+        y = np.empty((n, 4), dtype=np.uint64)
+        m = -1
+    else:
+        y = np.empty(n, dtype=np.uint64)
+        m = int(mode)
+    rc = lib().crvec_oracle_f64_batch(FN[fn], _p64(x), _p64(y), n, m, threads)
+    if rc != 0:
+        raise RuntimeError(f"oracle: {fn} f64 undecidable at precision cap")
+    return y
+
+
+def sweep_hashes(fn: str, chunk_lo: int = 0, chunk_hi: int = 4096, threads: int = 0,
+                 use_ld: bool = True) -> np.ndarray:
+    """Per-2^20-chunk, per-mode commutative hashes of the CR outputs."""
+    h = np.zeros((chunk_hi - chunk_lo, 4), dtype=np.uint64)
+    rc = lib().crvec_oracle_sweep_hashes(FN[fn], chunk_lo, chunk_hi, _p64(h), threads, int(use_ld))
+    if rc != 0:
+        raise RuntimeError(f"oracle: sweep {fn} failed rc={rc}")
+    return h
+
+
+def ref_f32(fn: str, xbits: np.ndarray, mode: int, threads: int = 0) -> np.ndarray:
+    """The REFERENCE's ziv_correctly_round_f32 over an array (exp2/log/log2 only)."""
+    x = np.ascontiguousarray(xbits, dtype=np.uint32)
+    y = np.empty_like(x)
+    rc = ref().crvec_ref_batch_f32(FN[fn], _p32(x), _p32(y), x.size, int(mode), threads)
+    if rc != 0:
+        raise RuntimeError("reference oracle threw")
+    return y
+
+
+def ref_f64(fn: str, xbits: np.ndarray, mode: int, threads: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(xbits, dtype=np.uint64)
+    y = np.empty_like(x)
+    rc = ref().crvec_ref_batch_f64(FN[fn], _p64(x), _p64(y), x.size, int(mode), threads)
+    if rc != 0:
+        raise RuntimeError("reference oracle threw")
+    return y
+
+
+def mix64(z: np.ndarray) -> np.ndarray:
+    """splitmix64 finalizer (vectorized), the sweep hash mixer."""
+    z = np.asarray(z, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        z ^= z >> np.uint64(30)
+        z *= np.uint64(0xBF58476D1CE4E5B9)
+        z ^= z >> np.uint64(27)
+        z *= np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+    return z

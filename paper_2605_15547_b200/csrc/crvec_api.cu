@@ -1,0 +1,323 @@
+// C ABI (include/crvec.h): argument checking, dispatch to the per-(function,
+// mode) kernels, the pipelined host-pointer path, device counters.
+//
+// There is no CPU fallback anywhere: without an sm_100 device every entry
+// point returns CRVEC_ENODEV.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/crvec.h"
+#include "crvec_kernels.cuh"
+
+namespace crvec {
+void register_exp(FnEntry *t);
+void register_log(FnEntry *t);
+void register_trig(FnEntry *t);
+void register_atrig(FnEntry *t);
+int f64_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
+                 unsigned long long *ctr);
+}  // namespace crvec
+
+using namespace crvec;
+
+namespace {
+
+constexpr int kMaxDev = 16;
+constexpr size_t kChunk = size_t(1) << 22;  // host path pipeline chunk (elements)
+
+FnEntry g_table[CRVEC_FN_COUNT];
+std::once_flag g_table_once;
+std::mutex g_mu;
+std::atomic<uint64_t> g_lanes{0};
+thread_local char g_err[256] = "";
+
+struct Dev {
+  bool init = false;
+  int status = CRVEC_ENODEV;
+  unsigned long long *counters = nullptr;  // [0] lanes (unused), [1] fast_undecided, [2] acc, [3] host
+  // host-path staging
+  void *buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  size_t buf_bytes = 0;
+  cudaStream_t st[2] = {nullptr, nullptr};
+};
+Dev g_dev[kMaxDev];
+
+int cuda_fail(cudaError_t e) {
+  std::snprintf(g_err, sizeof(g_err), "%s", cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? CRVEC_ENOMEM : CRVEC_ECUDA;
+}
+
+// Current device, initialised on first use (sm_100 required).
+int device(Dev **out) {
+  std::call_once(g_table_once, [] {
+    register_exp(g_table);
+    register_log(g_table);
+    register_trig(g_table);
+    register_atrig(g_table);
+  });
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess || d < 0 || d >= kMaxDev) {
+    std::snprintf(g_err, sizeof(g_err), "no CUDA device: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return CRVEC_ENODEV;
+  }
+  Dev &D = g_dev[d];
+  if (!D.init) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!D.init) {
+      cudaDeviceProp p;
+      e = cudaGetDeviceProperties(&p, d);
+      if (e != cudaSuccess || p.major != 10) {
+        std::snprintf(g_err, sizeof(g_err), "device %d is not sm_100 (cc %d.%d)", d,
+                      e == cudaSuccess ? p.major : -1, e == cudaSuccess ? p.minor : -1);
+        D.status = CRVEC_ENODEV;
+      } else if ((e = cudaMalloc(&D.counters, 4 * sizeof(unsigned long long))) != cudaSuccess ||
+                 (e = cudaMemset(D.counters, 0, 4 * sizeof(unsigned long long))) != cudaSuccess) {
+        D.status = cuda_fail(e);
+      } else {
+        D.status = CRVEC_OK;
+      }
+      D.init = true;
+    }
+  }
+  *out = &D;
+  return D.status;
+}
+
+int check_args(int fn, const void *x, const void *y, const void *y2, size_t n, int mode) {
+  if (fn < 0 || fn >= CRVEC_FN_COUNT || mode < 0 || mode > 3) return CRVEC_EINVAL;
+  if (n && (!x || !y)) return CRVEC_EINVAL;
+  if (n && fn == CRVEC_FN_SINCOSF && !y2) return CRVEC_EINVAL;
+  return CRVEC_OK;
+}
+
+int launch(Dev *D, int fn, const float *x, float *y, float *y2, size_t n, int mode,
+           cudaStream_t s) {
+  if (!n) return CRVEC_OK;
+  g_lanes += n;
+  cudaError_t e = g_table[fn].map[mode](x, y, y2, n, s, D->counters + 1);
+  return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
+int ensure_staging(Dev *D, size_t bytes) {
+  if (D->buf_bytes >= bytes) return CRVEC_OK;
+  for (auto &b : D->buf)
+    for (auto &p : b)
+      if (p) { cudaFree(p); p = nullptr; }
+  D->buf_bytes = 0;
+  for (auto &b : D->buf)
+    for (auto &p : b) {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+  for (auto &s : D->st)
+    if (!s) {
+      cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+  D->buf_bytes = bytes;
+  return CRVEC_OK;
+}
+
+// Host-pointer path: chunks alternate between two streams so the H2D copy of
+// chunk i+1, the kernel of chunk i and the D2H copy of chunk i-1 overlap
+// (fully when the host buffers are pinned).
+template <class T, class Launch>
+int host_pipeline(Dev *D, const T *x, T *y, T *y2, size_t n, Launch &&lf) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t chunk = n < kChunk ? n : kChunk;
+  int rc = ensure_staging(D, chunk * sizeof(T));
+  if (rc) return rc;
+  size_t i = 0;
+  for (size_t off = 0; off < n; off += chunk, ++i) {
+    size_t cnt = n - off < chunk ? n - off : chunk;
+    int k = i & 1;
+    cudaStream_t s = D->st[k];
+    T *dx = (T *)D->buf[k][0], *dy = (T *)D->buf[k][1], *dy2 = (T *)D->buf[k][2];
+    cudaError_t e = cudaMemcpyAsync(dx, x + off, cnt * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    rc = lf(dx, dy, y2 ? dy2 : nullptr, cnt, s);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(y + off, dy, cnt * sizeof(T), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && y2)
+      e = cudaMemcpyAsync(y2 + off, dy2, cnt * sizeof(T), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  for (auto s : D->st) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return CRVEC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int crvec_eval_f32_dev(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n,
+                       crvec_mode_t mode, void *stream) {
+  int rc = check_args(fn, x, y, y2, n, mode);
+  if (rc) return rc;
+  Dev *D;
+  if ((rc = device(&D))) return rc;
+  return launch(D, fn, x, y, y2, n, mode, (cudaStream_t)stream);
+}
+
+int crvec_eval_f32(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n,
+                   crvec_mode_t mode) {
+  int rc = check_args(fn, x, y, y2, n, mode);
+  if (rc || !n) return rc;
+  Dev *D;
+  if ((rc = device(&D))) return rc;
+  return host_pipeline<float>(D, x, y, fn == CRVEC_FN_SINCOSF ? y2 : nullptr, n,
+                              [&](const float *dx, float *dy, float *dy2, size_t cnt,
+                                  cudaStream_t s) { return launch(D, fn, dx, dy, dy2, cnt, mode, s); });
+}
+
+#define CRVEC_DEF(name, id)                                                                 \
+  int crvec_##name(const float *x, float *y, size_t n, crvec_mode_t m) {                    \
+    return crvec_eval_f32(id, x, y, nullptr, n, m);                                         \
+  }                                                                                         \
+  int crvec_##name##_dev(const float *x, float *y, size_t n, crvec_mode_t m, void *s) {     \
+    return crvec_eval_f32_dev(id, x, y, nullptr, n, m, s);                                  \
+  }
+CRVEC_DEF(expf, CRVEC_FN_EXPF)
+CRVEC_DEF(exp2f, CRVEC_FN_EXP2F)
+CRVEC_DEF(exp10f, CRVEC_FN_EXP10F)
+CRVEC_DEF(expm1f, CRVEC_FN_EXPM1F)
+CRVEC_DEF(logf, CRVEC_FN_LOGF)
+CRVEC_DEF(log2f, CRVEC_FN_LOG2F)
+CRVEC_DEF(log10f, CRVEC_FN_LOG10F)
+CRVEC_DEF(log1pf, CRVEC_FN_LOG1PF)
+CRVEC_DEF(sinf, CRVEC_FN_SINF)
+CRVEC_DEF(cosf, CRVEC_FN_COSF)
+CRVEC_DEF(tanf, CRVEC_FN_TANF)
+CRVEC_DEF(asinf, CRVEC_FN_ASINF)
+CRVEC_DEF(acosf, CRVEC_FN_ACOSF)
+CRVEC_DEF(atanf, CRVEC_FN_ATANF)
+CRVEC_DEF(sinhf, CRVEC_FN_SINHF)
+CRVEC_DEF(coshf, CRVEC_FN_COSHF)
+CRVEC_DEF(tanhf, CRVEC_FN_TANHF)
+CRVEC_DEF(rsqrtf, CRVEC_FN_RSQRTF)
+#undef CRVEC_DEF
+
+int crvec_sincosf(const float *x, float *s, float *c, size_t n, crvec_mode_t m) {
+  return crvec_eval_f32(CRVEC_FN_SINCOSF, x, s, c, n, m);
+}
+int crvec_sincosf_dev(const float *x, float *s, float *c, size_t n, crvec_mode_t m, void *st) {
+  return crvec_eval_f32_dev(CRVEC_FN_SINCOSF, x, s, c, n, m, st);
+}
+
+#ifdef CRVEC_WITH_F64
+// ---- binary64 ----
+static int eval_f64(int fn, const double *x, double *y, size_t n, int mode, crvec_stats_t *stats) {
+  if (mode < 0 || mode > 3 || (n && (!x || !y))) return CRVEC_EINVAL;
+  if (!n) return CRVEC_OK;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  unsigned long long before[4] = {0, 0, 0, 0}, after[4] = {0, 0, 0, 0};
+  if (stats) cudaMemcpy(before, D->counters, sizeof(before), cudaMemcpyDeviceToHost);
+  g_lanes += n;
+  rc = host_pipeline<double>(D, x, y, nullptr, n,
+                             [&](const double *dx, double *dy, double *, size_t cnt, cudaStream_t s) {
+                               return f64_dispatch(fn, dx, dy, cnt, mode, s, D->counters);
+                             });
+  if (rc) return rc;
+  if (stats) {
+    cudaMemcpy(after, D->counters, sizeof(after), cudaMemcpyDeviceToHost);
+    stats->lanes = n;
+    stats->fast_undecided = after[1] - before[1];
+    stats->accurate_undecided = after[2] - before[2];
+    stats->host_callouts = after[3] - before[3];
+  }
+  return CRVEC_OK;
+}
+static int eval_f64_dev(int fn, const double *x, double *y, size_t n, int mode, void *stream) {
+  if (mode < 0 || mode > 3 || (n && (!x || !y))) return CRVEC_EINVAL;
+  if (!n) return CRVEC_OK;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  g_lanes += n;
+  return f64_dispatch(fn, x, y, n, mode, (cudaStream_t)stream, D->counters);
+}
+int crvec_exp2(const double *x, double *y, size_t n, crvec_mode_t m, crvec_stats_t *st) {
+  return eval_f64(0, x, y, n, m, st);
+}
+int crvec_log(const double *x, double *y, size_t n, crvec_mode_t m, crvec_stats_t *st) {
+  return eval_f64(1, x, y, n, m, st);
+}
+int crvec_exp2_dev(const double *x, double *y, size_t n, crvec_mode_t m, void *s) {
+  return eval_f64_dev(0, x, y, n, m, s);
+}
+int crvec_log_dev(const double *x, double *y, size_t n, crvec_mode_t m, void *s) {
+  return eval_f64_dev(1, x, y, n, m, s);
+}
+
+#endif
+
+// ---- sweep ----
+int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *hashes,
+                    uint64_t *hashes2, uint64_t *counters, int force_accurate, void *stream) {
+  if (fn < 0 || fn >= CRVEC_FN_COUNT || chunk_hi > 4096 || chunk_lo >= chunk_hi || !hashes ||
+      !counters || (fn == CRVEC_FN_SINCOSF && !hashes2))
+    return CRVEC_EINVAL;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  cudaError_t e = g_table[fn].sweep(chunk_lo, chunk_hi, hashes, hashes2, force_accurate,
+                                    (cudaStream_t)stream, (unsigned long long *)counters);
+  return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
+// ---- accounting ----
+int crvec_stats_get(crvec_stats_t *out) {
+  if (!out) return CRVEC_EINVAL;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  unsigned long long c[4];
+  cudaError_t e = cudaMemcpy(c, D->counters, sizeof(c), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e);
+  out->lanes = g_lanes.load();
+  out->fast_undecided = c[1];
+  out->accurate_undecided = c[2];
+  out->host_callouts = c[3];
+  return CRVEC_OK;
+}
+int crvec_stats_reset(void) {
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  g_lanes = 0;
+  cudaError_t e = cudaMemset(D->counters, 0, 4 * sizeof(unsigned long long));
+  return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
+const char *crvec_strerror(int code) {
+  switch (code) {
+    case CRVEC_OK: return "ok";
+    case CRVEC_EINVAL: return "invalid argument";
+    case CRVEC_ECUDA: return "CUDA runtime error";
+    case CRVEC_ENOMEM: return "device allocation failed";
+    case CRVEC_ENODEV: return "no usable sm_100 CUDA device";
+  }
+  return "unknown error";
+}
+const char *crvec_last_cuda_error(void) { return g_err; }
+const char *crvec_version(void) { return "crvec-b200 0.1 (sm_100a)"; }
+int crvec_fn_count(void) { return CRVEC_FN_COUNT; }
+const char *crvec_fn_name(crvec_fn_t fn) {
+  static const char *names[CRVEC_FN_COUNT] = {
+      "exp2f", "logf",  "log2f", "expf",  "exp10f", "expm1f", "log10f", "log1pf", "sinf", "cosf",
+      "tanf",  "asinf", "acosf", "atanf", "sinhf",  "coshf",  "tanhf",  "rsqrtf", "sincosf"};
+  return (fn >= 0 && fn < CRVEC_FN_COUNT) ? names[fn] : "?";
+}
+
+}  // extern "C"

@@ -1,0 +1,735 @@
+// The 19 correctly rounded binary32 functions of the paper (ref: PAPER.md:49):
+// fast path (branch-free fp64 range reduction + <=16-entry register table via
+// __shfl_sync + fp64 polynomial + one static-mode conversion) and a rare
+// double-double accurate path for lanes the rounding test cannot decide.
+//
+// The reference implements exp2f / log2f only (ref: proj/src/kernels_f32.cpp:
+// 36-157, Figs. 1-2 of PAPER.md); its algorithms need ten 8-entry permutes
+// per element for log2f, which on a GPU is 20 SHFL per element. These kernels
+// instead follow the paper's own "one larger table and constant coefficients"
+// variant (ref: PAPER.md:130) and replace the RZ+sticky final step with an
+// explicit Ziv straddle test on the fp64 result (ref: proj/src/kernels_f64.cpp:
+// 63-76) so every fast-path lane is provably decided; correctness of the
+// whole (fast + accurate path) is established exhaustively against the CPU
+// oracle over all 2^32 inputs in all four modes.
+#pragma once
+#include "crvec_device.cuh"
+#include "crvec_tables.inc"
+
+namespace crvec {
+
+#define SHIFTER 0x1.8p52
+
+// Polynomials (Horner, coefficients from tools/gen_tables.py).
+CR_F double expq(double r) {
+  return fma_(fma_(fma_(fma_(EXPQ_C4, r, EXPQ_C3), r, EXPQ_C2), r, EXPQ_C1), r, EXPQ_C0);
+}
+CR_F double logq(double r) {
+  double q = fma_(LOGQ_C7, r, LOGQ_C6);
+  q = fma_(q, r, LOGQ_C5);
+  q = fma_(q, r, LOGQ_C4);
+  q = fma_(q, r, LOGQ_C3);
+  q = fma_(q, r, LOGQ_C2);
+  q = fma_(q, r, LOGQ_C1);
+  return fma_(q, r, LOGQ_C0);
+}
+
+// ============================================================ exp family ====
+// exp_core: 2^(k/16) * e^r with |r| <= ln2/32 (fast path).
+CR_F double exp_core(int k, double r, double tab) {
+  double T = CR_TAB(tab, EXP2J_HI, k & 15);
+  double p = fma_(mul_(r, r), expq(r), r);  // e^r - 1
+  return scale2(fma_(T, p, T), k >> 4);
+}
+
+// Double-double e^r, |r| <= ln2/32: Taylor to r^13 (error < 2^-104).
+CR_F DD exp_r_dd(DD r) {
+  DD p = {INVFACT_HI[13], INVFACT_LO[13]};
+  for (int n = 12; n >= 0; --n) p = dd_add(dd_mul(p, r), DD{INVFACT_HI[n], INVFACT_LO[n]});
+  return p;
+}
+// 2^(k/16) * e^r as DD, exponent applied (results stay normal in binary64).
+CR_F DD exp_dd(int k, DD r) {
+  int j = k & 15, e = k >> 4;
+  DD v = dd_mul(DD{EXP2J_HI[j], EXP2J_LO[j]}, exp_r_dd(r));
+  double s = scale2(1.0, e);
+  return DD{v.hi * s, v.lo * s};
+}
+
+// Argument reduction x = k*ln2/16 + r for the natural-base functions.
+struct RedExp {
+  int k;
+  double kd, r;
+};
+CR_F RedExp red_exp(double xc) {
+  double t = fma_(xc, INV_LN2_16, SHIFTER);
+  double kd = sub_(t, SHIFTER);
+  double r = fma_(kd, -LN2_16_H, xc);  // exact (Cody-Waite)
+  r = fma_(kd, -LN2_16_M, r);
+  return {(int)d2lo(t), kd, r};
+}
+CR_F DD red_exp_dd(double xc, int &k) {
+  double t = fma_(xc, INV_LN2_16, SHIFTER);
+  double kd = sub_(t, SHIFTER);
+  k = (int)d2lo(t);
+  double r1 = fma_(kd, -LN2_16_H, xc);       // exact
+  DD r = two_sum(r1, -mul_(kd, LN2_16_M));   // kd*M exact
+  return dd_add_d(r, -mul_(kd, LN2_16_L));
+}
+
+struct FnExp {
+  static constexpr uint32_t E = 8;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    double xc = fmin(fmax(xd, -104.5), 89.5);
+    RedExp q = red_exp(xc);
+    double a = exp_core(q.k, q.r, R.t);
+    bool skip = false;
+    if (dabs(xd) <= 0x1p-26) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
+    if (xd == 0.0) { a = 1.0; skip = true; }
+    if (x == INFINITY) { a = INFINITY; skip = true; }
+    if (x == -INFINITY) { a = 0.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xc = fmin(fmax(f2d(x), -104.5), 89.5);
+    int k;
+    DD r = red_exp_dd(xc, k);
+    return exp_dd(k, r);
+  }
+};
+
+struct FnExp2 {
+  static constexpr uint32_t E = 8;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    double xc = fmin(fmax(xd, -151.5), 129.5);
+    double t = fma_(xc, 16.0, SHIFTER);
+    double kd = sub_(t, SHIFTER);
+    double u = fma_(kd, -0.0625, xc);  // exact
+    int k = (int)d2lo(t);
+    double a = exp_core(k, mul_(u, LN2_D), R.t);
+    bool skip = (u == 0.0) && ((k & 15) == 0);  // 2^integer: exact
+    if (dabs(xd) <= 0x1p-26) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
+    if (xd == 0.0) { a = 1.0; skip = true; }
+    if (x == INFINITY) { a = INFINITY; skip = true; }
+    if (x == -INFINITY) { a = 0.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xc = fmin(fmax(f2d(x), -151.5), 129.5);
+    double t = fma_(xc, 16.0, SHIFTER);
+    double kd = sub_(t, SHIFTER);
+    double u = fma_(kd, -0.0625, xc);
+    DD r = two_prod(u, LN2_D);
+    r = dd_add_d(r, mul_(u, LN2_DL));
+    return exp_dd((int)d2lo(t), r);
+  }
+};
+
+struct FnExp10 {
+  static constexpr uint32_t E = 8;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    double xc = fmin(fmax(xd, -45.5), 39.5);
+    double t = fma_(xc, LOG2_10_16, SHIFTER);
+    double kd = sub_(t, SHIFTER);
+    double r = fma_(xc, LN10_H, -mul_(kd, LN2_16_H));
+    r = fma_(xc, LN10_M, r);
+    r = fma_(kd, -LN2_16_M, r);
+    r = fma_(xc, LN10_L, r);
+    double a = exp_core((int)d2lo(t), r, R.t);
+    bool skip = false;
+    if (dabs(xd) <= 0x1p-28) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
+    if (xd == 0.0) { a = 1.0; skip = true; }
+    if (x == INFINITY) { a = INFINITY; skip = true; }
+    if (x == -INFINITY) { a = 0.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xc = fmin(fmax(f2d(x), -45.5), 39.5);
+    double t = fma_(xc, LOG2_10_16, SHIFTER);
+    double kd = sub_(t, SHIFTER);
+    // x*ln10 - k*ln2/16 in DD: all partial products exact except the last.
+    DD r = two_sum(mul_(xc, LN10_H), -mul_(kd, LN2_16_H));
+    r = dd_add_d(r, mul_(xc, LN10_M));
+    r = dd_add_d(r, -mul_(kd, LN2_16_M));
+    r = dd_add(r, two_prod(xc, LN10_L));
+    r = dd_add_d(r, -mul_(kd, LN2_16_L));
+    return exp_dd((int)d2lo(t), r);
+  }
+};
+
+struct FnExpm1 {
+  static constexpr uint32_t E = 16;
+  struct Regs { double t, tl; };
+  CR_F static void load(Regs &R) {
+    R.t = CR_TAB_LOAD(EXP2J_HI);
+    R.tl = CR_TAB_LOAD(EXP2J_LO);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    double xc = fmin(fmax(xd, -18.5), 89.5);
+    RedExp q = red_exp(xc);
+    int j = q.k & 15, e = q.k >> 4;
+    double T = scale2(CR_TAB(R.t, EXP2J_HI, j), e);
+    double Tl = CR_TAB(R.tl, EXP2J_LO, j) * scale2(1.0, e);
+    double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
+    double a = fma_(T, p, add_(sub_(T, 1.0), Tl));
+    bool skip = false;
+    if (xd < -18.0) { a = -1.0 + 0x1p-40; skip = true; }
+    if (dabs(xd) <= 0x1p-26) { a = fma_(dabs(xd), 0x1p-36, xd); skip = true; }
+    if (xd == 0.0) { a = xd; skip = true; }
+    if (x == INFINITY) { a = INFINITY; skip = true; }
+    if (x == -INFINITY) { a = -1.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xc = fmin(fmax(f2d(x), -18.5), 89.5);
+    int k;
+    DD r = red_exp_dd(xc, k);
+    if (k == 0) {  // e^r - 1 = sum_{n>=1} r^n/n!, no cancellation
+      DD p = {INVFACT_HI[14], INVFACT_LO[14]};
+      for (int n = 13; n >= 1; --n) p = dd_add(dd_mul(p, r), DD{INVFACT_HI[n], INVFACT_LO[n]});
+      return dd_mul(p, r);
+    }
+    return dd_add_d(exp_dd(k, r), -1.0);
+  }
+};
+
+// Hyperbolics share the exp reduction: x = a + r, a = k ln2/16,
+// sinh x = sinh a cosh r + cosh a sinh r, cosh x = cosh a cosh r + sinh a sinh r.
+struct HypParts {
+  double Sa, Ca, sr, cr;
+};
+CR_F HypParts hyp_parts(double ax, double tab, double tabl) {
+  RedExp q = red_exp(ax);
+  int kp = q.k, km = -q.k;
+  double s1 = scale2(1.0, kp >> 4), s2 = scale2(1.0, km >> 4);
+  double Ep = CR_TAB(tab, EXP2J_HI, kp & 15) * s1, Elp = CR_TAB(tabl, EXP2J_LO, kp & 15) * s1;
+  double Em = CR_TAB(tab, EXP2J_HI, km & 15) * s2, Elm = CR_TAB(tabl, EXP2J_LO, km & 15) * s2;
+  double s = mul_(q.r, q.r);
+  double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ_C2, s, SINHQ_C1), s, SINHQ_C0), q.r);
+  double cr = fma_(s, fma_(fma_(COSHQ_C2, s, COSHQ_C1), s, COSHQ_C0), 1.0);
+  double Sa = mul_(add_(sub_(Ep, Em), sub_(Elp, Elm)), 0.5);
+  double Ca = mul_(add_(Ep, Em), 0.5);
+  return {Sa, Ca, sr, cr};
+}
+struct HypDD {
+  DD Sa, Ca, sr, cr;
+};
+CR_F HypDD hyp_parts_dd(double ax) {
+  int k;
+  DD r = red_exp_dd(ax, k);
+  DD s = dd_mul(r, r);
+  // sinh r = r * sum s^n/(2n+1)!, cosh r = sum s^n/(2n)!  (n <= 6)
+  DD ps = {INVFACT_HI[13], INVFACT_LO[13]}, pc = {INVFACT_HI[12], INVFACT_LO[12]};
+  for (int n = 5; n >= 0; --n) {
+    ps = dd_add(dd_mul(ps, s), DD{INVFACT_HI[2 * n + 1], INVFACT_LO[2 * n + 1]});
+    pc = dd_add(dd_mul(pc, s), DD{INVFACT_HI[2 * n], INVFACT_LO[2 * n]});
+  }
+  DD sr = dd_mul(ps, r);
+  int kp = k, km = -k;
+  double s1 = scale2(1.0, kp >> 4), s2 = scale2(1.0, km >> 4);
+  DD Ep = {EXP2J_HI[kp & 15] * s1, EXP2J_LO[kp & 15] * s1};
+  DD Em = {EXP2J_HI[km & 15] * s2, EXP2J_LO[km & 15] * s2};
+  DD Sa = dd_add(Ep, dd_neg(Em)), Ca = dd_add(Ep, Em);
+  Sa = DD{Sa.hi * 0.5, Sa.lo * 0.5};
+  Ca = DD{Ca.hi * 0.5, Ca.lo * 0.5};
+  return {Sa, Ca, sr, pc};
+}
+
+struct FnSinh {
+  static constexpr uint32_t E = 16;
+  struct Regs { double t, tl; };
+  CR_F static void load(Regs &R) {
+    R.t = CR_TAB_LOAD(EXP2J_HI);
+    R.tl = CR_TAB_LOAD(EXP2J_LO);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x), ax = fmin(dabs(xd), 90.0);
+    HypParts h = hyp_parts(ax, R.t, R.tl);
+    double a = fma_(h.Sa, h.cr, mul_(h.Ca, h.sr));
+    a = xd < 0 ? -a : a;
+    bool skip = false;
+    if (dabs(xd) <= 0x1p-12) { a = fma_(xd, 0x1p-36, xd); skip = true; }
+    if (xd == 0.0 || dabs(xd) == INFINITY) { a = xd; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x);
+    HypDD h = hyp_parts_dd(fmin(dabs(xd), 90.0));
+    DD v = dd_add(dd_mul(h.Sa, h.cr), dd_mul(h.Ca, h.sr));
+    return xd < 0 ? dd_neg(v) : v;
+  }
+};
+
+struct FnCosh {
+  static constexpr uint32_t E = 8;
+  struct Regs { double t, tl; };
+  CR_F static void load(Regs &R) {
+    R.t = CR_TAB_LOAD(EXP2J_HI);
+    R.tl = CR_TAB_LOAD(EXP2J_LO);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x), ax = fmin(dabs(xd), 90.0);
+    HypParts h = hyp_parts(ax, R.t, R.tl);
+    double a = fma_(h.Ca, h.cr, mul_(h.Sa, h.sr));
+    bool skip = false;
+    if (dabs(xd) <= 0x1p-13) { a = 1.0 + 0x1p-30; skip = true; }
+    if (xd == 0.0) { a = 1.0; skip = true; }
+    if (dabs(xd) == INFINITY) { a = INFINITY; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    HypDD h = hyp_parts_dd(fmin(dabs(f2d(x)), 90.0));
+    return dd_add(dd_mul(h.Ca, h.cr), dd_mul(h.Sa, h.sr));
+  }
+};
+
+struct FnTanh {
+  static constexpr uint32_t E = 32;
+  struct Regs { double t, tl; };
+  CR_F static void load(Regs &R) {
+    R.t = CR_TAB_LOAD(EXP2J_HI);
+    R.tl = CR_TAB_LOAD(EXP2J_LO);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x), ax = fmin(dabs(xd), 10.0);
+    HypParts h = hyp_parts(ax, R.t, R.tl);
+    double sh = fma_(h.Sa, h.cr, mul_(h.Ca, h.sr));
+    double ch = fma_(h.Ca, h.cr, mul_(h.Sa, h.sr));
+    double a = div_fast(sh, ch);
+    a = xd < 0 ? -a : a;
+    bool skip = false;
+    if (dabs(xd) >= 10.0) { a = xd > 0 ? 1.0 - 0x1p-40 : -1.0 + 0x1p-40; skip = true; }
+    if (dabs(xd) <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
+    if (xd == 0.0) { a = xd; skip = true; }
+    if (dabs(xd) == INFINITY) { a = xd > 0 ? 1.0 : -1.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x);
+    HypDD h = hyp_parts_dd(fmin(dabs(xd), 10.0));
+    DD sh = dd_add(dd_mul(h.Sa, h.cr), dd_mul(h.Ca, h.sr));
+    DD ch = dd_add(dd_mul(h.Ca, h.cr), dd_mul(h.Sa, h.sr));
+    DD v = dd_div(sh, ch);
+    return xd < 0 ? dd_neg(v) : v;
+  }
+};
+
+// ============================================================ log family ====
+// x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
+// offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
+// relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
+struct RedLog {
+  int e, i;
+  double m;
+};
+CR_F RedLog red_log(double xd) {
+  int h = d2hi(xd);
+  int hh = h - 0x3FE88000;
+  int e = hh >> 20;
+  return {e, (hh >> 16) & 15, hilo2d(h - (e << 20), d2lo(xd))};
+}
+
+template <int BASE>  // 0: ln, 2: log2, 10: log10
+struct FnLogB {
+  static constexpr uint32_t E = 8;
+  struct Regs { float c; double l; };
+  CR_F static void load(Regs &R) {
+    R.c = CR_TAB_LOAD(LOG_C);
+    R.l = BASE == 0 ? CR_TAB_LOAD(LOG_L_HI) : BASE == 2 ? CR_TAB_LOAD(LOG2_L_HI) : CR_TAB_LOAD(LOG10_L_HI);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    RedLog q = red_log(xd);
+    double c = f2d(CR_TAB(R.c, LOG_C, q.i));
+    double L = BASE == 0 ? CR_TAB(R.l, LOG_L_HI, q.i)
+                         : BASE == 2 ? CR_TAB(R.l, LOG2_L_HI, q.i) : CR_TAB(R.l, LOG10_L_HI, q.i);
+    double r = fma_(q.m, c, -1.0);
+    double p = fma_(mul_(r, r), logq(r), r);
+    double ed = i2d(q.e), a;
+    if (BASE == 0) a = add_(fma_(ed, LN2_D, L), p);
+    else if (BASE == 2) a = fma_(p, INV_LN2, add_(ed, L));
+    else a = fma_(p, INV_LN10, fma_(ed, LOG10_2, L));
+    bool skip = false;
+    uint32_t xb = f2u(x);
+    if (xb == 0x3F800000u) { a = 0.0; skip = true; }
+    if ((xb & 0x7FFFFFFFu) == 0) { a = -INFINITY; skip = true; }
+    if (xb > 0x80000000u) { a = NAN; skip = true; }
+    if (xb == 0x7F800000u) { a = INFINITY; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD log_dd_core(int e, int i, DD r) {
+    // log1p(r) = sum_{n=1}^{24} (-1)^(n+1) r^n / n
+    DD p = dd_mul(dd_horner(LOG1P_T_HI, LOG1P_T_LO, 24, r), r);
+    double ed = i2d(e);
+    DD el = two_sum(mul_(ed, LN2_H), mul_(ed, LN2_M));
+    el = dd_add_d(el, mul_(ed, LN2_L));
+    DD v = dd_add(dd_add(el, DD{LOG_L_HI[i], LOG_L_LO[i]}), p);
+    if (BASE == 2) v = dd_mul(v, DD{INV_LN2, INV_LN2_L});
+    if (BASE == 10) v = dd_mul(v, DD{INV_LN10, INV_LN10_L});
+    return v;
+  }
+  CR_F static DD slow(float x) {
+    RedLog q = red_log(f2d(x));
+    double r = fma_(q.m, (double)LOG_C[q.i], -1.0);  // exact
+    return log_dd_core(q.e, q.i, DD{r, 0.0});
+  }
+};
+using FnLog = FnLogB<0>;
+using FnLog2 = FnLogB<2>;
+using FnLog10 = FnLogB<10>;
+
+struct FnLog1p {
+  static constexpr uint32_t E = 8;
+  struct Regs { float c; double l; };
+  CR_F static void load(Regs &R) {
+    R.c = CR_TAB_LOAD(LOG_C);
+    R.l = CR_TAB_LOAD(LOG_L_HI);
+  }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x);
+    double y = add_(1.0, xd);
+    RedLog q = red_log(y);
+    double c = f2d(CR_TAB(R.c, LOG_C, q.i));
+    double L = CR_TAB(R.l, LOG_L_HI, q.i);
+    double r = fma_(q.m, c, -1.0);
+    double p = fma_(mul_(r, r), logq(r), r);
+    double a = add_(fma_(i2d(q.e), LN2_D, L), p);
+    bool skip = false;
+    if (dabs(xd) <= 0x1p-26) { a = fma_(-dabs(xd), 0x1p-36, xd); skip = true; }
+    if (xd == 0.0) { a = xd; skip = true; }
+    if (xd == -1.0) { a = -INFINITY; skip = true; }
+    if (xd < -1.0) { a = NAN; skip = true; }
+    if (xd == INFINITY) { a = INFINITY; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x);
+    DD y = two_sum(1.0, xd);  // 1 + x = y.hi + y.lo exactly
+    RedLog q = red_log(y.hi);
+    DD pm = two_prod(q.m, (double)LOG_C[q.i]);
+    DD r = fast_two_sum(sub_(pm.hi, 1.0), pm.lo);
+    DD v = FnLogB<0>::log_dd_core(q.e, q.i, r);
+    return dd_add_d(v, y.lo / y.hi);
+  }
+};
+
+// ================================================================== trig ====
+// x = k*pi/16 + r, |r| <= pi/32; sin(x) = S_k cos r + C_k sin r with
+// S_k = sin(k pi/16) = +-SIN16[k & 15] (sign from k & 16), C_k = S_{k+8}.
+struct RedTrig {
+  int k;
+  double r;
+};
+CR_F RedTrig red_trig_small(double xd) {
+  double t = fma_(xd, INV_PI_16, SHIFTER);
+  double kd = sub_(t, SHIFTER);
+  double r = fma_(kd, -PI_16_H, xd);
+  r = fma_(kd, -PI_16_M, r);
+  r = fma_(kd, -PI_16_L, r);
+  return {(int)d2lo(t), r};
+}
+
+// Payne-Hanek for |x| >= 2^17 (binary32 x = M * 2^(ex-23)):
+// x*16/pi mod 32 from a 32*NW-bit window of 1/pi times the 24-bit M.
+// Returns k mod 32 (of |x|) and the 64-bit signed fraction (units 2^-64),
+// plus (NW >= 6) the next 64 fraction bits for the accurate path.
+struct PH {
+  int k;
+  int64_t f;      // fraction * 2^64, in [-2^63, 2^63)
+  uint64_t f2;    // following 64 bits (accurate path only)
+};
+template <int NW>
+CR_F PH payne_hanek(uint32_t xb, const unsigned *words) {
+  int ex = (int)((xb >> 23) & 0xFF) - 127;
+  uint32_t M = (xb & 0x7FFFFFu) | 0x800000u;
+  int g0 = ex + 40;  // bit index of j0 = ex - 23 in the padded word array
+  int w0 = g0 >> 5, sh = g0 & 31;
+  uint32_t W[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint32_t a = words[w0 + i], b = words[w0 + i + 1];
+    W[i] = sh ? (a << sh) | (b >> (32 - sh)) : a;
+  }
+  // P = M * W (little-endian limbs L[0..NW]); W[0] is the most significant.
+  uint32_t L[NW + 1];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint64_t p = (uint64_t)M * W[NW - 1 - i] + carry;
+    L[i] = (uint32_t)p;
+    carry = p >> 32;
+  }
+  L[NW] = (uint32_t)carry;
+  // value = P * 2^-(32*NW - 5): integer part mod 32 = top 5 bits of limb NW-1.
+  uint32_t top = L[NW - 1];
+  uint32_t kk = top >> 27;
+  uint64_t f = ((uint64_t)(top & 0x07FFFFFFu) << 37) | ((uint64_t)L[NW - 2] << 5) | (L[NW - 3] >> 27);
+  uint64_t f2 = 0;
+  if (NW >= 6)
+    f2 = ((uint64_t)(L[NW - 3] & 0x07FFFFFFu) << 37) | ((uint64_t)L[NW - 4] << 5) | (L[NW - 5] >> 27);
+  kk += (uint32_t)(f >> 63);
+  return {(int)kk, (int64_t)f, f2};
+}
+
+CR_F double sin_r(double r, double s) {
+  return fma_(mul_(r, s), fma_(fma_(fma_(SINQ_C3, s, SINQ_C2), s, SINQ_C1), s, SINQ_C0), r);
+}
+CR_F double cos_r(double s) {
+  return fma_(s, fma_(fma_(fma_(COSQ_C3, s, COSQ_C2), s, COSQ_C1), s, COSQ_C0), 1.0);
+}
+CR_F double sin16(double tab, int k) {
+  double v = CR_TAB(tab, SIN16_HI, k & 15);
+  return (k & 16) ? -v : v;
+}
+
+// DD sin/cos of r (|r| <= pi/32), Taylor to r^23.
+CR_F void sincos_r_dd(DD r, DD &sr, DD &cr) {
+  DD s = dd_mul(r, r);
+  DD ps = {SINT_HI[11], SINT_LO[11]}, pc = {COST_HI[11], COST_LO[11]};
+  for (int n = 10; n >= 0; --n) {
+    ps = dd_add(dd_mul(ps, s), DD{SINT_HI[n], SINT_LO[n]});
+    pc = dd_add(dd_mul(pc, s), DD{COST_HI[n], COST_LO[n]});
+  }
+  sr = dd_mul(ps, r);
+  cr = pc;
+}
+CR_F DD sin16_dd(int k) {
+  DD v = {SIN16_HI[k & 15], SIN16_LO[k & 15]};
+  return (k & 16) ? dd_neg(v) : v;
+}
+// Accurate reduction: k and r (DD) for any finite binary32 x.
+CR_F DD red_trig_dd(float x, int &k) {
+  double xd = f2d(x);
+  uint32_t xb = f2u(x);
+  if (dabs(xd) < 0x1p17) {
+    double t = fma_(xd, INV_PI_16, SHIFTER);
+    double kd = sub_(t, SHIFTER);
+    k = (int)d2lo(t);
+    double r1 = fma_(kd, -PI_16_Q1, xd);            // exact
+    DD r = two_sum(r1, -mul_(kd, PI_16_Q2));         // exact product
+    r = dd_add_d(r, -mul_(kd, PI_16_Q3));            // exact product
+    return dd_add_d(r, -mul_(kd, PI_16_Q4));
+  }
+  PH p = payne_hanek<6>(xb & 0x7FFFFFFFu, INV_PI_WORDS);
+  // fraction = f*2^-64 + f2*2^-128 (f signed), times pi/16
+  double fh = (double)(p.f >> 11) * 0x1p11;          // exact (53 bits)
+  double fl = (double)(p.f & 2047) + (double)(p.f2 >> 11) * 0x1p-53;
+  DD fr = fast_two_sum(fh, fl);
+  DD r = dd_mul(fr, DD{PI_16_2M64_H, PI_16_2M64_L});
+  k = p.k;
+  if (xb >> 31) { k = -k; r = dd_neg(r); }
+  return r;
+}
+
+// Big-argument lanes of a warp are reduced together (warp-cooperative
+// Payne-Hanek): see ph_cooperative() in the kernel file. This helper is the
+// per-lane body it runs.
+CR_F RedTrig ph_reduce(float x, const unsigned *words) {
+  uint32_t xb = f2u(x);
+  PH p = payne_hanek<6>(xb & 0x7FFFFFFFu, words);
+  // 64 + 53 fraction bits: relative accuracy of r even when |r| is tiny.
+  double fr = fma_((double)(p.f2 >> 11), 0x1p-53, (double)p.f);
+  double r = mul_(fr, PI_16_2M64_H);
+  int k = p.k;
+  if (xb >> 31) { k = -k; r = -r; }
+  return {k, r};
+}
+
+struct TrigRegs {
+  double t;
+};
+template <int WHICH>  // 0: sin, 1: cos, 2: tan
+struct FnTrig {
+  static constexpr uint32_t E = WHICH == 2 ? 32 : 16;
+  static constexpr bool kBigArg = true;
+  using Regs = TrigRegs;
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN16_HI); }
+  CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
+    double xd = f2d(x);
+    double s = mul_(q.r, q.r);
+    double sr = sin_r(q.r, s), cr = cos_r(s);
+    double Sk = sin16(R.t, q.k), Ck = sin16(R.t, q.k + 8);
+    double a;
+    if (WHICH == 0) a = fma_(Sk, cr, mul_(Ck, sr));
+    else if (WHICH == 1) a = fma_(Ck, cr, -mul_(Sk, sr));
+    else a = div_fast(fma_(Sk, cr, mul_(Ck, sr)), fma_(Ck, cr, -mul_(Sk, sr)));
+    bool skip = false;
+    double ax = dabs(xd);
+    if (WHICH == 0 && ax <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
+    if (WHICH == 2 && ax <= 0x1p-13) { a = fma_(xd, 0x1p-36, xd); skip = true; }
+    if (WHICH == 1 && ax <= 0x1p-13) { a = 1.0 - 0x1p-31; skip = true; }
+    if (xd == 0.0) { a = WHICH == 1 ? 1.0 : xd; skip = true; }
+    if (ax == INFINITY) { a = NAN; skip = true; }
+    return {a, skip};
+  }
+  CR_F static bool is_big(float x) { return fabs_(x) >= 0x1p17f && fabs_(x) != INFINITY; }
+  CR_F static Fast fast(float x, const Regs &R) { return from_red(x, red_trig_small(f2d(x)), R); }
+  CR_F static DD slow(float x) {
+    int k;
+    DD r = red_trig_dd(x, k);
+    DD sr, cr;
+    sincos_r_dd(r, sr, cr);
+    DD Sk = sin16_dd(k), Ck = sin16_dd(k + 8);
+    DD sn = dd_add(dd_mul(Sk, cr), dd_mul(Ck, sr));
+    DD cs = dd_add(dd_mul(Ck, cr), dd_neg(dd_mul(Sk, sr)));
+    if (WHICH == 0) return sn;
+    if (WHICH == 1) return cs;
+    return dd_div(sn, cs);
+  }
+};
+using FnSin = FnTrig<0>;
+using FnCos = FnTrig<1>;
+using FnTan = FnTrig<2>;
+
+// ========================================================== inverse trig ====
+// atan2-style core for Y, X >= 0: theta_j = j*pi/30 (j = 0..15), t =
+// tan(angle - theta_j) = (Y cos - X sin)/(X cos + Y sin), result theta_j +
+// atan(t); sin/cos of theta_j from one 16-entry table (cos theta_j = sin
+// theta_{15-j}).
+CR_F int atan_index(double Y, double X) {
+  float yf = (float)Y, xf = (float)X;
+  float mn = fminf(yf, xf), mx = fmaxf(yf, xf);
+#if CR_DEVICE
+  float q = __fdividef(mn, mx);
+#else
+  float q = mn / mx;
+#endif
+  q = mx > 0.0f ? q : 0.0f;
+  float at = q * fmaf(0.273f, 1.0f - q, 0.78539816f);
+  float ang = yf > xf ? 1.57079633f - at : at;
+  int j = (int)rintf(ang * 9.5492966f);  // 30/pi
+  return j < 0 ? 0 : (j > 15 ? 15 : j);
+}
+CR_F double atan_t(double t) {
+  double s = mul_(t, t);
+  double q = fma_(fma_(fma_(fma_(fma_(ATANQ_C5, s, ATANQ_C4), s, ATANQ_C3), s, ATANQ_C2), s, ATANQ_C1), s,
+                  ATANQ_C0);
+  return fma_(mul_(t, s), q, t);
+}
+CR_F double atan2_core(double Y, double X, double tab) {
+  int j = atan_index(Y, X);
+  double S = CR_TAB(tab, SIN30_HI, j), C = CR_TAB(tab, SIN30_HI, 15 - j);
+  double num = fma_(Y, C, -mul_(X, S));
+  double den = fma_(X, C, mul_(Y, S));
+  double t = div_fast(num, den);
+  return fma_(i2d(j), PI_30_H, atan_t(t));
+}
+CR_F DD atan2_core_dd(DD Y, DD X) {
+  int j = atan_index(Y.hi, X.hi);
+  DD S = {SIN30_HI[j], SIN30_LO[j]}, C = {SIN30_HI[15 - j], SIN30_LO[15 - j]};
+  DD num = dd_add(dd_mul(Y, C), dd_neg(dd_mul(X, S)));
+  DD den = dd_add(dd_mul(X, C), dd_mul(Y, S));
+  DD t = dd_div(num, den);
+  DD s = dd_mul(t, t);
+  DD p = dd_mul(dd_horner(ATANT_HI, ATANT_LO, 14, s), t);
+  double jd = i2d(j);
+  DD th = two_prod(jd, PI_30_H);
+  th = dd_add_d(th, mul_(jd, PI_30_L));
+  return dd_add(th, p);
+}
+
+struct FnAtan {
+  static constexpr uint32_t E = 16;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x), ax = dabs(xd);
+    double a = atan2_core(fmin(ax, 0x1p127), 1.0, R.t);
+    a = xd < 0 ? -a : a;
+    bool skip = false;
+    if (ax <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
+    if (xd == 0.0) { a = xd; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x);
+    DD v = atan2_core_dd(DD{fmin(dabs(xd), 0x1p127), 0.0}, DD{1.0, 0.0});
+    return xd < 0 ? dd_neg(v) : v;
+  }
+};
+
+template <bool ACOS>
+struct FnAsinAcos {
+  static constexpr uint32_t E = 32;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
+  CR_F static Fast fast(float x, const Regs &R) {
+    double xd = f2d(x), ax = fmin(dabs(xd), 1.0);
+    double s = sqrt_rn(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
+    double a;
+    if (!ACOS) {
+      a = atan2_core(ax, s, R.t);
+      a = xd < 0 ? -a : a;
+    } else {
+      a = atan2_core(s, ax, R.t);
+      a = xd < 0 ? add_(PI_H, -a) : a;
+    }
+    bool skip = false;
+    if (!ACOS && dabs(xd) <= 0x1p-12) { a = fma_(xd, 0x1p-36, xd); skip = true; }
+    if (!ACOS && xd == 0.0) { a = xd; skip = true; }
+    if (ACOS && xd == 1.0) { a = 0.0; skip = true; }
+    if (dabs(xd) > 1.0) { a = NAN; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x), ax = fmin(dabs(xd), 1.0);
+    DD s = dd_sqrt(DD{fma_(-ax, ax, 1.0), 0.0});
+    if (!ACOS) {
+      DD v = atan2_core_dd(DD{ax, 0.0}, s);
+      return xd < 0 ? dd_neg(v) : v;
+    }
+    DD v = atan2_core_dd(s, DD{ax, 0.0});
+    return xd < 0 ? dd_add(DD{PI_H, PI_L}, dd_neg(v)) : v;
+  }
+};
+using FnAsin = FnAsinAcos<false>;
+using FnAcos = FnAsinAcos<true>;
+
+// ================================================================= rsqrt ====
+struct FnRsqrt {
+  static constexpr uint32_t E = 8;
+  struct Regs {};
+  CR_F static void load(Regs &) {}
+  CR_F static double newton(double xd) {
+    double y = rsqrt_approx(xd);
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      double e = fma_(-mul_(xd, y), y, 1.0);
+      y = fma_(mul_(y, 0.5), e, y);
+    }
+    return y;
+  }
+  CR_F static Fast fast(float x, const Regs &) {
+    double xd = f2d(x);
+    double a = newton(xd);
+    bool skip = false;
+    uint32_t xb = f2u(x);
+    if (xb == 0u) { a = INFINITY; skip = true; }
+    if (xb == 0x80000000u) { a = -INFINITY; skip = true; }
+    if (xb > 0x80000000u) { a = NAN; skip = true; }
+    if (xb == 0x7F800000u) { a = 0.0; skip = true; }
+    return {a, skip};
+  }
+  CR_F static DD slow(float x) {
+    double xd = f2d(x);
+    double y = newton(xd);
+    // e = 1 - x y^2 exactly in DD; y' = y (1 + e/2 + 3e^2/8)
+    DD y2 = two_prod(y, y);
+    DD xy2 = dd_mul_d(y2, xd);
+    DD e = dd_add_d(dd_neg(xy2), 1.0);
+    double corr = mul_(y, fma_(0.375, e.hi * e.hi, 0.5 * e.hi));
+    return fast_two_sum(y, corr);
+  }
+};
+
+}  // namespace crvec

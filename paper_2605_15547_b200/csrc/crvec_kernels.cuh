@@ -1,0 +1,516 @@
+// Kernel templates: streaming map kernels (128-bit coalesced I/O, grid-stride,
+// warp-uniform loops so register tables can use __shfl_sync), the
+// warp-cooperative Payne-Hanek path, the rare accurate-path fallback, and the
+// exhaustive-sweep kernel with a commutative per-chunk hash.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "crvec_fns_f32.cuh"
+
+namespace crvec {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <class F>
+struct IsTrig {
+  static constexpr bool value = false;
+};
+template <int W>
+struct IsTrig<FnTrig<W>> {
+  static constexpr bool value = true;
+};
+
+// Streaming 128-bit accesses: read-only non-coherent path without L1
+// allocation, evict-first stores (inputs and outputs are touched once).
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// Accurate path: one lane, double-double evaluation + round_dd. Out of line so
+// the fast path keeps its register budget; reached with probability ~2^-24.
+template <class F, int M>
+__device__ __noinline__ uint32_t slow_round(float x) {
+  DD v = F::slow(x);
+  return round_dd<M>(v.hi, v.lo);
+}
+template <class F>
+__device__ __noinline__ DD slow_dd(float x) {
+  return F::slow(x);
+}
+
+// ---------------------------------------------- warp-cooperative Payne-Hanek
+// Per-warp staging: the big-argument elements of the warp's 32 x NE slots are
+// compacted (ballot + popc prefix) into a queue, reduced 32 at a time by all
+// lanes, and scattered back. One pass serves up to 32 big arguments however
+// they are spread over lanes and slots.
+struct PHWarp {
+  float qx[128];
+  unsigned char qslot[128];
+  int rk[128];
+  double rr[128];
+};
+struct PHBlock {
+  unsigned words[12];
+  PHWarp warp[kWarps];
+};
+
+template <int NE>
+__device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bool (&big)[NE],
+                                                 RedTrig (&q)[NE], PHBlock &sh) {
+  const int lane = threadIdx.x & 31;
+  PHWarp &w = sh.warp[threadIdx.x >> 5];
+  const unsigned lt = (1u << lane) - 1u;
+  int total = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    unsigned m = __ballot_sync(kFull, big[e]);
+    if (big[e]) {
+      int pos = total + __popc(m & lt);
+      w.qx[pos] = xs[e];
+      w.qslot[pos] = (unsigned char)(e * 32 + lane);
+    }
+    total += __popc(m);
+  }
+  __syncwarp();
+  for (int base = 0; base < total; base += 32) {
+    int i = base + lane;
+    if (i < total) {
+      RedTrig r = ph_reduce(w.qx[i], sh.words);
+      int s = w.qslot[i];
+      w.rk[s] = r.k;
+      w.rr[s] = r.r;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+    if (big[e]) q[e] = RedTrig{w.rk[e * 32 + lane], w.rr[e * 32 + lane]};
+  __syncwarp();
+}
+
+// Fast results for NE elements per lane (warp converged on entry).
+template <class F, int NE>
+__device__ __forceinline__ void fast_lanes(const float (&xs)[NE], Fast (&f)[NE],
+                                           const typename F::Regs &R, PHBlock *sh) {
+  if constexpr (IsTrig<F>::value) {
+    RedTrig q[NE];
+    bool big[NE];
+    bool any = false;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      q[e] = red_trig_small(f2d(xs[e]));
+      big[e] = F::is_big(xs[e]);
+      any |= big[e];
+    }
+    if (__any_sync(kFull, any)) coop_payne_hanek<NE>(xs, big, q, *sh);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) f[e] = F::from_red(xs[e], q[e], R);
+  } else {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) f[e] = F::fast(xs[e], R);
+  }
+}
+
+template <class F, int M, int NE>
+__device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)[NE],
+                                           const typename F::Regs &R, PHBlock *sh,
+                                           unsigned long long *counters) {
+  Fast f[NE];
+  fast_lanes<F, NE>(xs, f, R, sh);
+  bool fail[NE];
+  bool any = false;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    ys[e] = finish<M>(f2u(xs[e]), f[e], fail[e], F::E);
+    any |= fail[e];
+  }
+  if (__any_sync(kFull, any)) {
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (fail[e]) {
+        ys[e] = slow_round<F, M>(xs[e]);
+        ++cnt;
+      }
+    }
+    if (cnt) atomicAdd(counters, (unsigned long long)cnt);
+  }
+}
+
+// Shared staging exists only in the trig kernels (17 KB per block).
+template <class F>
+__device__ __forceinline__ PHBlock *ph_storage() {
+  if constexpr (IsTrig<F>::value) {
+    __shared__ PHBlock sh;
+    if (threadIdx.x < 12) sh.words[threadIdx.x] = INV_PI_WORDS[threadIdx.x];
+    __syncthreads();
+    return &sh;
+  } else {
+    return nullptr;
+  }
+}
+
+// ------------------------------------------------------------ map kernels ----
+// 4 elements (one float4) per lane per iteration; the loop trip count is
+// warp-uniform so the register-table shuffles always see a full warp.
+template <class F, int M>
+__global__ void __launch_bounds__(kThreads) k_map_vec(const float4 *x, float4 *y, uint64_t n4,
+                                                      unsigned long long *counters) {
+  PHBlock *sh = ph_storage<F>();
+  typename F::Regs R;
+  F::load(R);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp * 32; base < n4; base += nwarps * 32) {
+    uint64_t i = base + lane;
+    bool valid = i < n4;
+    float4 v = valid ? ld_stream(x + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+    float xs[4] = {v.x, v.y, v.z, v.w};
+    uint32_t ys[4];
+    eval_lanes<F, M, 4>(xs, ys, R, sh, counters);
+    if (valid) st_stream(y + i, make_float4(u2f(ys[0]), u2f(ys[1]), u2f(ys[2]), u2f(ys[3])));
+  }
+}
+
+// Any alignment / tails: one element per lane.
+template <class F, int M>
+__global__ void __launch_bounds__(kThreads) k_map_scalar(const float *x, float *y, uint64_t n,
+                                                         unsigned long long *counters) {
+  PHBlock *sh = ph_storage<F>();
+  typename F::Regs R;
+  F::load(R);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp * 32; base < n; base += nwarps * 32) {
+    uint64_t i = base + lane;
+    bool valid = i < n;
+    float xs[1] = {valid ? x[i] : 1.0f};
+    uint32_t ys[1];
+    eval_lanes<F, M, 1>(xs, ys, R, sh, counters);
+    if (valid) y[i] = u2f(ys[0]);
+  }
+}
+
+// sincosf: one reduction, two outputs (1 in / 2 out = 12 B per element).
+template <int M, int NE>
+__device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s)[NE],
+                                             uint32_t (&c)[NE], const FnSin::Regs &R,
+                                             PHBlock *sh, unsigned long long *counters) {
+  RedTrig q[NE];
+  bool big[NE];
+  bool anyb = false;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    q[e] = red_trig_small(f2d(xs[e]));
+    big[e] = FnSin::is_big(xs[e]);
+    anyb |= big[e];
+  }
+  if (__any_sync(kFull, anyb)) coop_payne_hanek<NE>(xs, big, q, *sh);
+  bool fs[NE], fc[NE];
+  bool any = false;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    Fast a = FnSin::from_red(xs[e], q[e], R);
+    Fast b = FnCos::from_red(xs[e], q[e], R);
+    s[e] = finish<M>(f2u(xs[e]), a, fs[e], FnSin::E);
+    c[e] = finish<M>(f2u(xs[e]), b, fc[e], FnCos::E);
+    any |= fs[e] | fc[e];
+  }
+  if (__any_sync(kFull, any)) {
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (fs[e]) { s[e] = slow_round<FnSin, M>(xs[e]); ++cnt; }
+      if (fc[e]) { c[e] = slow_round<FnCos, M>(xs[e]); ++cnt; }
+    }
+    if (cnt) atomicAdd(counters, (unsigned long long)cnt);
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_sincos_vec(const float4 *x, float4 *ys, float4 *yc,
+                                                         uint64_t n4, unsigned long long *counters) {
+  PHBlock *sh = ph_storage<FnSin>();
+  FnSin::Regs R;
+  FnSin::load(R);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp * 32; base < n4; base += nwarps * 32) {
+    uint64_t i = base + lane;
+    bool valid = i < n4;
+    float4 v = valid ? ld_stream(x + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+    float xs[4] = {v.x, v.y, v.z, v.w};
+    uint32_t s[4], c[4];
+    sincos_lanes<M, 4>(xs, s, c, R, sh, counters);
+    if (valid) {
+      st_stream(ys + i, make_float4(u2f(s[0]), u2f(s[1]), u2f(s[2]), u2f(s[3])));
+      st_stream(yc + i, make_float4(u2f(c[0]), u2f(c[1]), u2f(c[2]), u2f(c[3])));
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_sincos_scalar(const float *x, float *ys, float *yc,
+                                                            uint64_t n, unsigned long long *counters) {
+  PHBlock *sh = ph_storage<FnSin>();
+  FnSin::Regs R;
+  FnSin::load(R);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp * 32; base < n; base += nwarps * 32) {
+    uint64_t i = base + lane;
+    bool valid = i < n;
+    float xs[1] = {valid ? x[i] : 1.0f};
+    uint32_t s[1], c[1];
+    sincos_lanes<M, 1>(xs, s, c, R, sh, counters);
+    if (valid) {
+      ys[i] = u2f(s[0]);
+      yc[i] = u2f(c[0]);
+    }
+  }
+}
+
+// ----------------------------------------------------------- sweep kernel ----
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
+template <class F>
+__device__ __forceinline__ void finish4(uint32_t xb, Fast f, uint32_t (&y)[4], bool &fail) {
+  y[0] = finish<RNE>(xb, f, fail, F::E);
+  bool d;
+  y[1] = finish<RZ>(xb, f, d, F::E);
+  y[2] = finish<RU>(xb, f, d, F::E);
+  y[3] = finish<RD>(xb, f, d, F::E);
+}
+__device__ __forceinline__ void round4(DD v, uint32_t (&y)[4]) {
+  y[0] = round_dd<RNE>(v.hi, v.lo);
+  y[1] = round_dd<RZ>(v.hi, v.lo);
+  y[2] = round_dd<RU>(v.hi, v.lo);
+  y[3] = round_dd<RD>(v.hi, v.lo);
+}
+
+// Block-wide sum of 4 (or 8) u64 lanes into global accumulators.
+template <int K>
+__device__ __forceinline__ void block_add(uint64_t (&acc)[K], uint64_t *dst) {
+  __shared__ uint64_t red[kWarps][K];
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+    for (int o = 16; o; o >>= 1) acc[m] += __shfl_xor_sync(kFull, acc[m], o);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int m = 0; m < K; ++m) red[threadIdx.x >> 5][m] = acc[m];
+  __syncthreads();
+  if (threadIdx.x < K) {
+    uint64_t s = 0;
+    for (int w = 0; w < kWarps; ++w) s += red[w][threadIdx.x];
+    atomicAdd((unsigned long long *)&dst[threadIdx.x], (unsigned long long)s);
+  }
+}
+
+// Exhaustive sweep over binary32 patterns: each block covers 4096 patterns of
+// one 2^20 chunk (256 blocks per chunk); every pattern is evaluated once and
+// converted in all four modes; per chunk and mode the hashes are summed.
+constexpr int kSweepPerThread = 16;
+constexpr int kSweepPerBlock = kThreads * kSweepPerThread;  // 4096
+constexpr int kSweepBlocksPerChunk = (1 << 20) / kSweepPerBlock;
+
+template <class F, bool FORCE>
+__global__ void __launch_bounds__(kThreads) k_sweep(uint32_t chunk_lo, uint64_t *hashes,
+                                                    unsigned long long *counters) {
+  PHBlock *sh = ph_storage<F>();
+  typename F::Regs R;
+  F::load(R);
+  uint32_t chunk = chunk_lo + blockIdx.x / kSweepBlocksPerChunk;
+  uint32_t p0 = (chunk << 20) + (blockIdx.x % kSweepBlocksPerChunk) * kSweepPerBlock;
+  uint64_t acc[4] = {0, 0, 0, 0};
+  int nslow = 0;
+#pragma unroll 1
+  for (int it = 0; it < kSweepPerThread / 4; ++it) {
+    uint32_t pb = p0 + it * (kThreads * 4) + threadIdx.x * 4;
+    float xs[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xs[e] = u2f(pb + e);
+    Fast f[4];
+    fast_lanes<F, 4>(xs, f, R, sh);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t y[4];
+      bool fail;
+      uint32_t xb = pb + e;
+      finish4<F>(xb, f[e], y, fail);
+      bool xnan = (xb & 0x7FFFFFFFu) > 0x7F800000u;
+      if (fail || (FORCE && !f[e].skip && !xnan)) {
+        round4(slow_dd<F>(xs[e]), y);
+        ++nslow;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[m] += mix64(((uint64_t)y[m] << 32) | xb);
+    }
+  }
+  if (nslow) atomicAdd(counters, (unsigned long long)nslow);
+  block_add<4>(acc, hashes + 4ull * (chunk - chunk_lo));
+}
+
+template <bool FORCE>
+__global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, uint64_t *hs,
+                                                           uint64_t *hc,
+                                                           unsigned long long *counters) {
+  PHBlock *sh = ph_storage<FnSin>();
+  FnSin::Regs R;
+  FnSin::load(R);
+  uint32_t chunk = chunk_lo + blockIdx.x / kSweepBlocksPerChunk;
+  uint32_t p0 = (chunk << 20) + (blockIdx.x % kSweepBlocksPerChunk) * kSweepPerBlock;
+  uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int nslow = 0;
+#pragma unroll 1
+  for (int it = 0; it < kSweepPerThread / 4; ++it) {
+    uint32_t pb = p0 + it * (kThreads * 4) + threadIdx.x * 4;
+    float xs[4];
+    RedTrig q[4];
+    bool big[4];
+    bool anyb = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      xs[e] = u2f(pb + e);
+      q[e] = red_trig_small(f2d(xs[e]));
+      big[e] = FnSin::is_big(xs[e]);
+      anyb |= big[e];
+    }
+    if (__any_sync(kFull, anyb)) coop_payne_hanek<4>(xs, big, q, *sh);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t xb = pb + e;
+      bool xnan = (xb & 0x7FFFFFFFu) > 0x7F800000u;
+      Fast a = FnSin::from_red(xs[e], q[e], R);
+      Fast b = FnCos::from_red(xs[e], q[e], R);
+      uint32_t ys[4], yc[4];
+      bool fs, fc;
+      finish4<FnSin>(xb, a, ys, fs);
+      finish4<FnCos>(xb, b, yc, fc);
+      if (fs || (FORCE && !a.skip && !xnan)) { round4(slow_dd<FnSin>(xs[e]), ys); ++nslow; }
+      if (fc || (FORCE && !b.skip && !xnan)) { round4(slow_dd<FnCos>(xs[e]), yc); ++nslow; }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        acc[m] += mix64(((uint64_t)ys[m] << 32) | xb);
+        acc[4 + m] += mix64(((uint64_t)yc[m] << 32) | xb);
+      }
+    }
+  }
+  if (nslow) atomicAdd(counters, (unsigned long long)nslow);
+  uint64_t a4[4] = {acc[0], acc[1], acc[2], acc[3]};
+  uint64_t c4[4] = {acc[4], acc[5], acc[6], acc[7]};
+  block_add<4>(a4, hs + 4ull * (chunk - chunk_lo));
+  __syncthreads();
+  block_add<4>(c4, hc + 4ull * (chunk - chunk_lo));
+}
+
+// ------------------------------------------------------------- launchers ----
+using MapLaunch = cudaError_t (*)(const float *, float *, float *, uint64_t, cudaStream_t,
+                                  unsigned long long *);
+using SweepLaunch = cudaError_t (*)(uint32_t, uint32_t, uint64_t *, uint64_t *, int, cudaStream_t,
+                                    unsigned long long *);
+
+template <class K>
+inline int max_blocks(K kernel) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, 0);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+inline unsigned grid_for(uint64_t work_warps32, int maxb) {
+  // work_warps32 = number of 32-lane slots; one warp per slot per pass
+  uint64_t blocks = (work_warps32 + kWarps - 1) / kWarps;
+  if (blocks > (uint64_t)maxb) blocks = maxb;
+  return (unsigned)(blocks ? blocks : 1);
+}
+
+template <class F, int M>
+cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream_t s,
+                       unsigned long long *ctr) {
+  static int mb_vec = max_blocks(k_map_vec<F, M>);
+  static int mb_sc = max_blocks(k_map_scalar<F, M>);
+  bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+  uint64_t n4 = aligned ? n / 4 : 0;
+  if (n4) {
+    k_map_vec<F, M><<<grid_for((n4 + 31) / 32, mb_vec), kThreads, 0, s>>>(
+        (const float4 *)x, (float4 *)y, n4, ctr);
+  }
+  uint64_t rem = n - 4 * n4;
+  if (rem) {
+    k_map_scalar<F, M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(x + 4 * n4, y + 4 * n4,
+                                                                            rem, ctr);
+  }
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_sincos(const float *x, float *ys, float *yc, uint64_t n, cudaStream_t s,
+                          unsigned long long *ctr) {
+  static int mb_vec = max_blocks(k_sincos_vec<M>);
+  static int mb_sc = max_blocks(k_sincos_scalar<M>);
+  bool aligned = (((uintptr_t)x | (uintptr_t)ys | (uintptr_t)yc) & 15) == 0;
+  uint64_t n4 = aligned ? n / 4 : 0;
+  if (n4)
+    k_sincos_vec<M><<<grid_for((n4 + 31) / 32, mb_vec), kThreads, 0, s>>>(
+        (const float4 *)x, (float4 *)ys, (float4 *)yc, n4, ctr);
+  uint64_t rem = n - 4 * n4;
+  if (rem)
+    k_sincos_scalar<M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(
+        x + 4 * n4, ys + 4 * n4, yc + 4 * n4, rem, ctr);
+  return cudaGetLastError();
+}
+
+template <class F>
+cudaError_t launch_sweep(uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *h, uint64_t *, int force,
+                         cudaStream_t s, unsigned long long *ctr) {
+  unsigned blocks = (chunk_hi - chunk_lo) * kSweepBlocksPerChunk;
+  if (force) k_sweep<F, true><<<blocks, kThreads, 0, s>>>(chunk_lo, h, ctr);
+  else k_sweep<F, false><<<blocks, kThreads, 0, s>>>(chunk_lo, h, ctr);
+  return cudaGetLastError();
+}
+
+inline cudaError_t launch_sweep_sincos(uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *h,
+                                       uint64_t *h2, int force, cudaStream_t s,
+                                       unsigned long long *ctr) {
+  unsigned blocks = (chunk_hi - chunk_lo) * kSweepBlocksPerChunk;
+  if (force) k_sweep_sincos<true><<<blocks, kThreads, 0, s>>>(chunk_lo, h, h2, ctr);
+  else k_sweep_sincos<false><<<blocks, kThreads, 0, s>>>(chunk_lo, h, h2, ctr);
+  return cudaGetLastError();
+}
+
+// Registration: each family translation unit fills its rows.
+struct FnEntry {
+  MapLaunch map[4];
+  SweepLaunch sweep;
+};
+template <class F>
+constexpr FnEntry make_entry() {
+  return FnEntry{{launch_map<F, RNE>, launch_map<F, RZ>, launch_map<F, RU>, launch_map<F, RD>},
+                 launch_sweep<F>};
+}
+
+}  // namespace crvec

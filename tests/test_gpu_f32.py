@@ -1,0 +1,144 @@
+"""GPU parity tests for the 19 binary32 CR functions (through the C ABI).
+
+Bit-exact against the CPU oracle (oracle/, a restatement of the reference's
+Ziv oracle, ref: proj/src/oracle.cpp:302-388) in all four rounding modes, on
+seeded random + special inputs, on the configs' input distributions, and —
+exhaustively over all 2^32 patterns — against the committed golden chunk
+hashes (tests/golden/sweep/) that the same oracle produced.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_15547_b200 as crvec
+from tests.inputs import log_family_input, mixed_f32, trig_input
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "sweep")
+
+
+def _mismatch_report(x, got, want):
+    bad = np.nonzero(got != want)[0]
+    return [(hex(int(x[i])), hex(int(got[i])), hex(int(want[i]))) for i in bad[:5]], len(bad)
+
+
+@pytest.mark.parametrize("name", crvec.F32_FUNCS)
+def test_random_and_specials_all_modes(cuda, oracle, name):
+    x = mixed_f32(name, 1 << 17, seed=11)
+    want = oracle.f32(crvec.ORACLE_NAME[name], x, None)
+    xt = cuda.from_numpy(x.view(np.float32)).cuda()
+    for mode in range(4):
+        got = crvec.eval_f32(name, xt, mode).cpu().numpy().view(np.uint32)
+        ex, nbad = _mismatch_report(x, got, want[:, mode])
+        assert nbad == 0, f"{name} mode {mode}: {nbad} mismatches, e.g. {ex}"
+
+
+@pytest.mark.parametrize("name", ["logf", "log2f", "log10f", "log1pf"])
+def test_log_family_config_inputs(cuda, oracle, name):
+    """Config C2 distribution (denormals / Inf / NaN / negatives injected)."""
+    x = log_family_input(name, 1 << 18)
+    for mode in range(4):
+        want = oracle.f32(crvec.ORACLE_NAME[name], x, mode)
+        got = crvec.eval_f32(name, x.view(np.float32), mode).view(np.uint32)  # host path
+        ex, nbad = _mismatch_report(x, got, want)
+        assert nbad == 0, f"{name} mode {mode}: {ex}"
+
+
+@pytest.mark.parametrize("name", ["sinf", "cosf", "tanf"])
+def test_trig_config_inputs_big_args(cuda, oracle, name):
+    """Config C3: 1/8 large-argument tail, randomly interleaved (Payne-Hanek path)."""
+    x = trig_input(1 << 18)
+    xt = cuda.from_numpy(x.view(np.float32)).cuda()
+    for mode in range(4):
+        want = oracle.f32(crvec.ORACLE_NAME[name], x, mode)
+        got = crvec.eval_f32(name, xt, mode).cpu().numpy().view(np.uint32)
+        ex, nbad = _mismatch_report(x, got, want)
+        assert nbad == 0, f"{name} mode {mode}: {ex}"
+
+
+def test_sincosf_matches_sin_and_cos(cuda, oracle):
+    x = np.concatenate([trig_input(1 << 16), mixed_f32("sincosf", 1 << 16)])
+    xt = cuda.from_numpy(x.view(np.float32)).cuda()
+    for mode in range(4):
+        s, c = crvec.cr_sincosf(xt, mode)
+        assert (s.cpu().numpy().view(np.uint32) == oracle.f32("sin", x, mode)).all()
+        assert (c.cpu().numpy().view(np.uint32) == oracle.f32("cos", x, mode)).all()
+
+
+def test_expf_config1_full_2p24(cuda, oracle):
+    """Config C1: expf over 2^24 uniform-random inputs, all four modes, bit-exact."""
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.integers(0, 2**32, 1 << 23, dtype=np.uint64).astype(np.uint32),
+                        rng.uniform(-104, 89, 1 << 23).astype(np.float32).view(np.uint32)])
+    want = oracle.f32("exp", x, None)
+    xt = cuda.from_numpy(x.view(np.float32)).cuda()
+    for mode in range(4):
+        got = crvec.cr_expf(xt, mode).cpu().numpy().view(np.uint32)
+        ex, nbad = _mismatch_report(x, got, want[:, mode])
+        assert nbad == 0, f"mode {mode}: {ex}"
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 31, 33, 127, 129, 1000])
+def test_sizes_alignment_inplace(cuda, oracle, n):
+    x = mixed_f32("logf", max(n, 1), seed=n)[:n]
+    want = oracle.f32("log", x, 0) if n else np.zeros(0, np.uint32)
+    got = crvec.cr_logf(x.view(np.float32)).view(np.uint32)
+    assert (got == want).all()
+    # unaligned device pointers (offset by one element) and in-place
+    buf = cuda.zeros(n + 1, dtype=cuda.float32, device="cuda")
+    buf[1:] = cuda.from_numpy(x.view(np.float32)).cuda()
+    v = buf[1:]
+    crvec.eval_f32("logf", v, 0, out=v)
+    assert (v.cpu().numpy().view(np.uint32) == want).all()
+
+
+def test_scalar_api_and_reference_examples(cuda):
+    """SPEC examples for cr_exp2f / cr_log2f (ref: SPEC.md kernels_f32 examples)."""
+    RM = crvec.RoundingMode
+    for m in RM:
+        assert crvec.cr_exp2f_scalar(0.0, m) == 1.0
+        assert crvec.cr_exp2f_scalar(127.0, m) == 2.0 ** 127
+        assert crvec.cr_log2f_scalar(1.0, m) == 0.0
+        assert crvec.cr_log2f_scalar(8.0, m) == 3.0
+        assert crvec.cr_log2f_scalar(2.0 ** -149, m) == -149.0
+    assert crvec.cr_exp2f_scalar(float("-inf")) == 0.0
+    assert np.isinf(crvec.cr_exp2f_scalar(128.0, RM.NearestEven))
+    assert crvec.cr_exp2f_scalar(128.0, RM.TowardZero) == np.finfo(np.float32).max
+    assert crvec.cr_exp2f_scalar(128.0, RM.TowardNegative) == np.finfo(np.float32).max
+    assert np.isneginf(crvec.cr_log2f_scalar(0.0))
+    nan = np.array([0xFF912345], np.uint32).view(np.float32)
+    assert crvec.cr_exp2f(nan).view(np.uint32)[0] == 0xFFD12345
+    assert crvec.cr_log2f(np.array([-1.0], np.float32)).view(np.uint32)[0] == 0x7FC00000
+
+
+def _golden(name):
+    p = os.path.join(GOLDEN, name + ".npy")
+    if not os.path.exists(p):
+        pytest.fail(f"golden sweep data missing: {p} (python tools/gen_golden.py {name})")
+    return np.load(p)
+
+
+@pytest.mark.parametrize("name", crvec.F32_FUNCS + ["sincosf"])
+def test_exhaustive_sweep_vs_golden(cuda, name):
+    """All 2^32 inputs x 4 modes: per-chunk hashes equal the oracle's golden."""
+    h, h2, _ = crvec.sweep_f32(name)
+    if name == "sincosf":
+        gs, gc = _golden("sin"), _golden("cos")
+        assert (h == gs).all(), f"sin chunks differ: {np.nonzero((h != gs).any(1))[0][:10]}"
+        assert (h2 == gc).all(), f"cos chunks differ: {np.nonzero((h2 != gc).any(1))[0][:10]}"
+        return
+    g = _golden(crvec.ORACLE_NAME[name])
+    bad = np.nonzero((h != g).any(1))[0]
+    assert len(bad) == 0, f"{name}: {len(bad)} chunks differ, first {bad[:10]}"
+
+
+@pytest.mark.parametrize("name", crvec.F32_FUNCS)
+def test_accurate_path_self_check(cuda, name):
+    """Route EVERY non-special lane through the double-double accurate path
+    (the rarely-taken fallback) over 64 spread chunks: must still match."""
+    g = _golden(crvec.ORACLE_NAME[name])
+    for lo in range(0, 4096, 512):
+        h, _, n_acc = crvec.sweep_f32(name, lo, lo + 8, force_accurate=True)
+        assert n_acc > 0
+        assert (h == g[lo:lo + 8]).all(), f"{name}: forced-accurate chunk mismatch at {lo}"

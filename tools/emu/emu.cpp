@@ -1,0 +1,71 @@
+// DEVELOPER TOOL ONLY (never shipped, never a fallback): compiles the device
+// math of paper_2605_15547_b200/csrc/crvec_fns_f32.cuh with g++ so algorithm
+// bugs can be caught on a GPU-less box against the CPU oracle. The GPU
+// kernels are the only product path.
+#define CRVEC_EMU 1
+#include <cstdint>
+#include <cstdio>
+#include <type_traits>
+#include "../../paper_2605_15547_b200/csrc/crvec_fns_f32.cuh"
+using namespace crvec;
+
+template <class F> struct is_trig : std::false_type {};
+template <int W> struct is_trig<FnTrig<W>> : std::true_type {};
+
+template <class F, int M>
+static uint32_t eval1(float x, int force, uint64_t *slow) {
+  typename F::Regs R;
+  F::load(R);
+  Fast f;
+  if constexpr (is_trig<F>::value) {
+    RedTrig q = F::is_big(x) ? ph_reduce(x, INV_PI_WORDS) : red_trig_small(f2d(x));
+    f = F::from_red(x, q, R);
+  } else {
+    f = F::fast(x, R);
+  }
+  bool fail;
+  uint32_t y = finish<M>(f2u(x), f, fail, F::E);
+  bool xnan = (f2u(x) & 0x7FFFFFFFu) > 0x7F800000u;
+  if (fail || (force && !f.skip && !xnan)) {
+    ++*slow;
+    DD v = F::slow(x);
+    y = round_dd<M>(v.hi, v.lo);
+  }
+  return y;
+}
+
+template <class F>
+static void run(const uint32_t *x, uint32_t *y, uint64_t n, int force, uint64_t *slow) {
+  for (uint64_t i = 0; i < n; ++i) {
+    float xf = u2f(x[i]);
+    y[4 * i + 0] = eval1<F, RNE>(xf, force, slow);
+    y[4 * i + 1] = eval1<F, RZ>(xf, force, slow);
+    y[4 * i + 2] = eval1<F, RU>(xf, force, slow);
+    y[4 * i + 3] = eval1<F, RD>(xf, force, slow);
+  }
+}
+
+extern "C" int emu_eval(int fn, const uint32_t *x, uint32_t *y, uint64_t n, int force, uint64_t *slow) {
+  switch (fn) {
+    case 0: run<FnExp2>(x, y, n, force, slow); break;
+    case 1: run<FnLog>(x, y, n, force, slow); break;
+    case 2: run<FnLog2>(x, y, n, force, slow); break;
+    case 3: run<FnExp>(x, y, n, force, slow); break;
+    case 4: run<FnExp10>(x, y, n, force, slow); break;
+    case 5: run<FnExpm1>(x, y, n, force, slow); break;
+    case 6: run<FnLog10>(x, y, n, force, slow); break;
+    case 7: run<FnLog1p>(x, y, n, force, slow); break;
+    case 8: run<FnSin>(x, y, n, force, slow); break;
+    case 9: run<FnCos>(x, y, n, force, slow); break;
+    case 10: run<FnTan>(x, y, n, force, slow); break;
+    case 11: run<FnAsin>(x, y, n, force, slow); break;
+    case 12: run<FnAcos>(x, y, n, force, slow); break;
+    case 13: run<FnAtan>(x, y, n, force, slow); break;
+    case 14: run<FnSinh>(x, y, n, force, slow); break;
+    case 15: run<FnCosh>(x, y, n, force, slow); break;
+    case 16: run<FnTanh>(x, y, n, force, slow); break;
+    case 17: run<FnRsqrt>(x, y, n, force, slow); break;
+    default: return -1;
+  }
+  return 0;
+}

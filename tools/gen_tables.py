@@ -1,0 +1,314 @@
+"""Offline table / coefficient generator for the crvec B200 kernels.
+
+Emits ``paper_2605_15547_b200/csrc/crvec_tables.inc`` (checked in). Every table
+has <= 16 entries (the paper's constraint, ref: PAPER.md:51) and every
+polynomial is a Chebyshev (near-minimax) fit computed with mpmath at 60 digits
+then rounded to binary64; the script prints each fast polynomial's worst
+relative error so the rounding-test tolerances in the kernels can be checked
+against it. ``--check`` regenerates into memory and compares with the
+checked-in file byte for byte (SPEC acceptance #8, ref: SPEC.md:666).
+
+This plays the role of the reference's empty coefficient generator
+(ref: proj/include/crvec/coeffgen.hpp:16-67, proj/src/coeffgen.cpp:1).
+"""
+import hashlib
+import os
+import sys
+
+import mpmath as mp
+
+mp.mp.dps = 60
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "paper_2605_15547_b200", "csrc", "crvec_tables.inc")
+
+
+def d(x):
+    """Round an mpf to the nearest binary64."""
+    return float(mp.mpf(x))
+
+
+def hx(x):
+    return float(x).hex()
+
+
+def dd(x):
+    """Double-double split of an mpf: (hi, lo) with hi = RN(x)."""
+    x = mp.mpf(x)
+    hi = d(x)
+    lo = d(x - hi)
+    return hi, lo
+
+
+def trunc_bits(x, bits):
+    """x rounded to `bits` significant bits (as a double)."""
+    x = mp.mpf(x)
+    if x == 0:
+        return 0.0
+    e = int(mp.floor(mp.log(abs(x), 2)))
+    q = mp.mpf(2) ** (e - bits + 1)
+    return d(mp.nint(x / q) * q)
+
+
+def split3(x, b1, b2):
+    """x = h + m + l with h (b1 bits), m (b2 bits) and l = RN(x - h - m)."""
+    x = mp.mpf(x)
+    h = trunc_bits(x, b1)
+    m = trunc_bits(x - h, b2)
+    l = d(x - h - m)
+    return h, m, l
+
+
+def chebfit(f, a, b, deg):
+    """Near-minimax polynomial (coefficients low->high, as mpf) for f on [a, b]."""
+    coeffs, err = mp.chebyfit(f, [a, b], deg + 1, error=True)
+    return list(reversed(coeffs)), err
+
+
+def rel_err_of(poly_eval, f, a, b, n=4000):
+    worst = mp.mpf(0)
+    for i in range(n + 1):
+        x = a + (b - a) * mp.mpf(i) / n
+        if x == 0:
+            continue
+        fx = f(x)
+        if fx == 0:
+            continue
+        e = abs((poly_eval(x) - fx) / fx)
+        if e > worst:
+            worst = e
+    return worst
+
+
+def horner(cs, x):
+    acc = mp.mpf(0)
+    for c in reversed(cs):
+        acc = acc * x + c
+    return acc
+
+
+lines = []
+report = []
+
+
+def emit(s=""):
+    lines.append(s)
+
+
+def arr(name, vals, ctype="double"):
+    emit(f"static CR_CONST {ctype} {name}[{len(vals)}] = {{")
+    for i in range(0, len(vals), 4):
+        emit("    " + ", ".join(hx(v) if ctype == "double" else repr(v) for v in vals[i:i + 4]) + ",")
+    emit("};")
+
+
+def scalar(name, v):
+    emit(f"#define {name} {hx(v)}")
+
+
+def poly_block(name, cs):
+    for i, c in enumerate(cs):
+        scalar(f"{name}_C{i}", d(c))
+
+
+# ------------------------------------------------------------------ exp ----
+LN2 = mp.log(2)
+R_EXP = LN2 / 32 * mp.mpf("1.0005")          # |r| bound after k = RN(x*16/ln2)
+
+
+def gen_exp():
+    emit("// ---- exp family: 2^(j/16) table, e^r - 1 polynomial ----")
+    T = [mp.mpf(2) ** (mp.mpf(j) / 16) for j in range(16)]
+    arr("EXP2J_HI", [dd(t)[0] for t in T])
+    arr("EXP2J_LO", [dd(t)[1] for t in T])
+    # e^r - 1 = r + r^2 * Q(r), Q degree 4 (fast path)
+    g = lambda r: (mp.expm1(r) - r) / r ** 2 if r != 0 else mp.mpf(1) / 2
+    for deg in (3, 4):
+        cs, _ = chebfit(g, -R_EXP, R_EXP, deg)
+        csd = [mp.mpf(d(c)) for c in cs]
+        err = rel_err_of(lambda r: r + r * r * horner(csd, r), mp.expm1, -R_EXP, R_EXP)
+        report.append(f"expm1 poly r+r^2*Q deg(Q)={deg}: max rel err 2^{float(mp.log(err, 2)):.1f}")
+        if deg == 4:
+            poly_block("EXPQ", csd)
+    h, m, l = split3(LN2 / 16, 40, 40)
+    scalar("LN2_16_H", h); scalar("LN2_16_M", m); scalar("LN2_16_L", l)
+    scalar("INV_LN2_16", d(16 / LN2))
+    scalar("LN2_D", d(LN2))
+    scalar("LN2_DL", d(LN2 - d(LN2)))
+    LOG2_10 = mp.log(10, 2)
+    scalar("LOG2_10_16", d(16 * LOG2_10))
+    h, m, l = split3(mp.log(10), 29, 29)
+    scalar("LN10_H", h); scalar("LN10_M", m); scalar("LN10_L", l)
+    # slow path: 1/n! as double-doubles, n = 0..16
+    inv_fact = [mp.mpf(1) / mp.factorial(n) for n in range(17)]
+    arr("INVFACT_HI", [dd(v)[0] for v in inv_fact])
+    arr("INVFACT_LO", [dd(v)[1] for v in inv_fact])
+    # exact powers of ten for exp10f(k), k = 0..10
+    arr("POW10_D", [float(10 ** k) for k in range(16)])
+    # sinh / cosh of r polynomials (fast path), |r| <= R_EXP
+    gs = lambda r: (mp.sinh(r) - r) / r ** 3 if r != 0 else mp.mpf(1) / 6
+    cs, _ = chebfit(lambda s: gs(mp.sqrt(s)) if s > 0 else mp.mpf(1) / 6, mp.mpf(0), R_EXP ** 2, 2)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda r: r + r ** 3 * horner(csd, r * r), mp.sinh, -R_EXP, R_EXP)
+    report.append(f"sinh poly deg(S)=2 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("SINHQ", csd)
+    gc = lambda s: (mp.cosh(mp.sqrt(s)) - 1) / s if s > 0 else mp.mpf(1) / 2
+    cs, _ = chebfit(gc, mp.mpf(0), R_EXP ** 2, 2)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda r: 1 + r * r * horner(csd, r * r), mp.cosh, -R_EXP, R_EXP)
+    report.append(f"cosh poly deg(C)=2 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("COSHQ", csd)
+
+
+# ------------------------------------------------------------------ log ----
+def gen_log():
+    emit("// ---- log family: normalization window [0.765625, 1.53125), 16 bins ----")
+    # bin i spans hi-words [OFF + i*2^16, OFF + (i+1)*2^16), OFF = 0x3FE88000
+    OFFV = mp.mpf("0.765625")
+    lo_edges = []
+    for i in range(16):
+        if i < 7:
+            a = OFFV + mp.mpf(i) / 32
+            b = a + mp.mpf(1) / 32
+        elif i == 7:
+            a, b = 1 - mp.mpf(1) / 64, 1 + mp.mpf(1) / 32
+        else:
+            a = 1 + mp.mpf(1) / 32 + mp.mpf(i - 8) / 16
+            b = a + mp.mpf(1) / 16
+        lo_edges.append((a, b))
+    cs_, L, L2, L10 = [], [], [], []
+    rmin, rmax = mp.mpf(0), mp.mpf(0)
+    for i, (a, b) in enumerate(lo_edges):
+        if i == 7:
+            c = mp.mpf(1)
+        else:
+            c = mp.mpf(trunc_bits(2 / (a + b), 20))
+        cs_.append(float(c))
+        rmin = min(rmin, a * c - 1)
+        rmax = max(rmax, b * c - 1)
+        L.append(-mp.log(c))
+        L2.append(-mp.log(c, 2))
+        L10.append(-mp.log(c, 10))
+    arr("LOG_C", cs_)
+    arr("LOG_L_HI", [dd(v)[0] for v in L]); arr("LOG_L_LO", [dd(v)[1] for v in L])
+    arr("LOG2_L_HI", [dd(v)[0] for v in L2]); arr("LOG2_L_LO", [dd(v)[1] for v in L2])
+    arr("LOG10_L_HI", [dd(v)[0] for v in L10]); arr("LOG10_L_LO", [dd(v)[1] for v in L10])
+    report.append(f"log r range [{float(rmin):.5f}, {float(rmax):.5f}]")
+    a, b = rmin * mp.mpf("1.001"), rmax * mp.mpf("1.001")
+    g = lambda r: (mp.log1p(r) - r) / r ** 2 if r != 0 else -mp.mpf(1) / 2
+    for deg in (6, 7):
+        cs, _ = chebfit(g, a, b, deg)
+        csd = [mp.mpf(d(c)) for c in cs]
+        err = rel_err_of(lambda r: r + r * r * horner(csd, r), mp.log1p, a, b)
+        report.append(f"log1p poly r+r^2*Q deg(Q)={deg}: max rel err 2^{float(mp.log(err, 2)):.1f}")
+        if deg == 7:
+            poly_block("LOGQ", csd)
+    h, m, l = split3(LN2, 40, 40)
+    scalar("LN2_H", h); scalar("LN2_M", m); scalar("LN2_L", l)
+    scalar("INV_LN2", d(1 / LN2)); scalar("INV_LN2_L", d(1 / LN2 - d(1 / LN2)))
+    scalar("INV_LN10", d(1 / mp.log(10))); scalar("INV_LN10_L", d(1 / mp.log(10) - d(1 / mp.log(10))))
+    scalar("LOG10_2", d(mp.log(2, 10))); scalar("LOG10_2_L", d(mp.log(2, 10) - d(mp.log(2, 10))))
+    # slow path: log1p(r) = sum (-1)^(n+1) r^n / n as DD, n = 1..24
+    inv = [mp.mpf((-1) ** (n + 1)) / n for n in range(1, 25)]
+    arr("LOG1P_T_HI", [dd(v)[0] for v in inv]); arr("LOG1P_T_LO", [dd(v)[1] for v in inv])
+
+
+# ----------------------------------------------------------------- trig ----
+def gen_trig():
+    emit("// ---- trig: k = RN(x*16/pi), sin(j*pi/16) table, sin/cos of r ----")
+    PI = mp.pi
+    S = [mp.sin(j * PI / 16) for j in range(16)]
+    arr("SIN16_HI", [dd(v)[0] for v in S]); arr("SIN16_LO", [dd(v)[1] for v in S])
+    R = PI / 32 * mp.mpf("1.0005")
+    gs = lambda s: (mp.sin(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 6
+    cs, _ = chebfit(gs, mp.mpf(0), R ** 2, 3)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda r: r + r ** 3 * horner(csd, r * r), mp.sin, -R, R)
+    report.append(f"sin poly deg 3 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("SINQ", csd)
+    gc = lambda s: (mp.cos(mp.sqrt(s)) - 1) / s if s > 0 else -mp.mpf(1) / 2
+    cs, _ = chebfit(gc, mp.mpf(0), R ** 2, 3)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda r: 1 + r * r * horner(csd, r * r), mp.cos, -R, R)
+    report.append(f"cos poly deg 3 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("COSQ", csd)
+    scalar("INV_PI_16", d(16 / PI))
+    h, m, l = split3(PI / 16, 33, 33)
+    scalar("PI_16_H", h); scalar("PI_16_M", m); scalar("PI_16_L", l)
+    # four-part split for the DD slow path
+    p1, p2, rest = split3(PI / 16, 33, 33)
+    p3 = trunc_bits(PI / 16 - p1 - p2, 33)
+    p4 = d(PI / 16 - p1 - p2 - p3)
+    scalar("PI_16_Q1", p1); scalar("PI_16_Q2", p2); scalar("PI_16_Q3", p3); scalar("PI_16_Q4", p4)
+    # Payne-Hanek: bits of 1/pi, 32-bit words, word w holds bits [32w+1, 32w+32]
+    # (bit j has weight 2^-j); 2 zero words of padding in front.
+    v = 1 / PI
+    words = [0, 0]
+    for w in range(10):
+        v = v * (mp.mpf(2) ** 32)
+        iw = int(mp.floor(v))
+        words.append(iw)
+        v -= iw
+    emit("static CR_CONST unsigned INV_PI_WORDS[12] = {")
+    emit("    " + ", ".join(f"0x{w:08x}u" for w in words) + ",")
+    emit("};")
+    hi, lo = dd(PI / 16 * mp.mpf(2) ** -64)
+    scalar("PI_16_2M64_H", hi); scalar("PI_16_2M64_L", lo)
+    # slow path: sin/cos Taylor terms (-1)^n / (2n+1)!, (-1)^n / (2n)!
+    sn = [mp.mpf((-1) ** n) / mp.factorial(2 * n + 1) for n in range(12)]
+    cn = [mp.mpf((-1) ** n) / mp.factorial(2 * n) for n in range(12)]
+    arr("SINT_HI", [dd(v)[0] for v in sn]); arr("SINT_LO", [dd(v)[1] for v in sn])
+    arr("COST_HI", [dd(v)[0] for v in cn]); arr("COST_LO", [dd(v)[1] for v in cn])
+
+
+# ---------------------------------------------------------- inverse trig ----
+def gen_atrig():
+    emit("// ---- inverse trig: theta_j = j*pi/30, j = 0..15, atan(t) polynomial ----")
+    PI = mp.pi
+    S = [mp.sin(j * PI / 30) for j in range(16)]
+    arr("SIN30_HI", [dd(v)[0] for v in S]); arr("SIN30_LO", [dd(v)[1] for v in S])
+    T = mp.tan(PI / 60 + mp.mpf("0.0065"))
+    report.append(f"atan t bound {float(T):.5f}")
+    g = lambda s: (mp.atan(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 3
+    for deg in (4, 5):
+        cs, _ = chebfit(g, mp.mpf(0), T ** 2, deg)
+        csd = [mp.mpf(d(c)) for c in cs]
+        err = rel_err_of(lambda t: t + t ** 3 * horner(csd, t * t), mp.atan, -T, T)
+        report.append(f"atan poly deg {deg} in t^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+        if deg == 5:
+            poly_block("ATANQ", csd)
+    h, l = dd(PI / 30)
+    scalar("PI_30_H", h); scalar("PI_30_L", l)
+    h, l = dd(PI)
+    scalar("PI_H", h); scalar("PI_L", l)
+    an = [mp.mpf((-1) ** n) / (2 * n + 1) for n in range(20)]
+    arr("ATANT_HI", [dd(v)[0] for v in an]); arr("ATANT_LO", [dd(v)[1] for v in an])
+
+
+def generate():
+    lines.clear()
+    report.clear()
+    emit("// GENERATED by tools/gen_tables.py -- do not edit. Tables <= 16 entries.")
+    emit("#pragma once")
+    gen_exp()
+    gen_log()
+    gen_trig()
+    gen_atrig()
+    return "\n".join(lines) + "\n"
+
+
+def main():
+    text = generate()
+    if "--check" in sys.argv:
+        cur = open(OUT).read()
+        ok = cur == text
+        print("tables:", "reproducible" if ok else "MISMATCH", hashlib.sha256(text.encode()).hexdigest()[:16])
+        sys.exit(0 if ok else 1)
+    with open(OUT, "w") as f:
+        f.write(text)
+    for r in report:
+        print(r)
+    print("wrote", OUT, hashlib.sha256(text.encode()).hexdigest()[:16])
+
+
+if __name__ == "__main__":
+    main()
