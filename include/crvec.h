@@ -123,6 +123,12 @@ int crvec_eval_f32(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n,
 int crvec_eval_f32_dev(crvec_fn_t fn, const float *x, float *y, float *y2, size_t n,
                        crvec_mode_t mode, void *stream);
 
+/* ---- binary64 exp2 / log (fast path + ballot-compacted accurate path) ---- */
+int crvec_exp2(const double *x, double *y, size_t n, crvec_mode_t mode, crvec_stats_t *stats);
+int crvec_log(const double *x, double *y, size_t n, crvec_mode_t mode, crvec_stats_t *stats);
+int crvec_exp2_dev(const double *x, double *y, size_t n, crvec_mode_t mode, void *stream);
+int crvec_log_dev(const double *x, double *y, size_t n, crvec_mode_t mode, void *stream);
+
 /* ---- exhaustive binary32 sweep (verify) ----
  * For chunks [chunk_lo, chunk_hi) of 2^20 bit patterns (chunk c = patterns
  * c<<20 .. (c<<20)+2^20-1), adds into hashes[(c - chunk_lo)*4 + mode]

@@ -29,6 +29,9 @@
 
 namespace crvec {
 
+// 1.5 * 2^52: adding it rounds to an integer kept in the low mantissa bits.
+#define SHIFTER 0x1.8p52
+
 // RoundingMode numbering of ref: proj/include/crvec/fpbits.hpp:13-18.
 enum : int { RNE = 0, RZ = 1, RU = 2, RD = 3 };
 
@@ -61,6 +64,7 @@ CR_F double rsqrt_approx(double x) {
   return r;
 }
 CR_F double sqrt_rn(double x) { return __dsqrt_rn(x); }
+CR_F int clz32(uint32_t v) { return __clz((int)v); }
 template <int M>
 CR_F float cvt_f32(double a) {
   if (M == RNE) return __double2float_rn(a);
@@ -87,6 +91,7 @@ CR_F float fabs_(float a) { return std::fabs(a); }
 CR_F double rcp_approx(double x) { return (double)(float)(1.0 / x); }
 CR_F double rsqrt_approx(double x) { return (double)(float)(1.0 / std::sqrt(x)); }
 CR_F double sqrt_rn(double x) { return std::sqrt(x); }
+CR_F int clz32(uint32_t v) { return v ? __builtin_clz(v) : 32; }
 template <int M>
 CR_F float cvt_f32(double a) {
   float f = (float)a;  // RNE with gradual underflow / overflow to inf

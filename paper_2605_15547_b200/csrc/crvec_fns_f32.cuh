@@ -18,7 +18,6 @@
 
 namespace crvec {
 
-#define SHIFTER 0x1.8p52
 
 // Polynomials (Horner, coefficients from tools/gen_tables.py).
 CR_F double expq(double r) {

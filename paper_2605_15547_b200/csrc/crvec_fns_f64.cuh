@@ -1,0 +1,412 @@
+// Correctly rounded binary64 exp2 and log (the two double-precision functions
+// of SPEC.md, ref: PAPER.md II.B, proj/src/kernels_f64.cpp:234-307).
+//
+//  fast path   the paper's algorithms in double-double: exp2 via
+//              x = N + (i1*256 + i2*16 + i3)/4096 + R and three 16-entry DD
+//              tables (ref: kernels_f64.cpp:82-100,135-150); log via a
+//              7-bit reciprocal, a 128-entry -log(rcp) DD table and a
+//              log1p(r) series (ref: kernels_f64.cpp:102-124).
+//  round test  Ziv straddle test in registers (ref: kernels_f64.cpp:63-76):
+//              the DD value +- eps|v| must round to the same binary64.
+//  accurate    lanes the test cannot decide (or whose result is subnormal)
+//              are compacted per warp with __ballot_sync into a side queue and
+//              evaluated by full warps in 256-bit fixed point (error < 2^-230,
+//              far below the binary64 worst cases of these functions), then
+//              rounded exactly. This replaces the reference's scalar MPFR
+//              callout (ref: kernels_f64.cpp:78-80); there is no host callout.
+#pragma once
+#include "crvec_device.cuh"
+#include "crvec_tables.inc"
+
+namespace crvec {
+
+// ------------------------------------------------- 256-bit fixed point ----
+// Signed two's complement, value = W / 2^240 (16 integer bits), w[0] least
+// significant.
+struct Fx {
+  uint32_t w[8];
+};
+constexpr int FX_FRAC = 240;
+
+CR_F Fx fx_zero() {
+  Fx r;
+  for (int i = 0; i < 8; ++i) r.w[i] = 0;
+  return r;
+}
+CR_F bool fx_neg_p(const Fx &a) { return (a.w[7] >> 31) != 0; }
+CR_F bool fx_is_zero(const Fx &a) {
+  uint32_t o = 0;
+  for (int i = 0; i < 8; ++i) o |= a.w[i];
+  return o == 0;
+}
+CR_F Fx fx_add(const Fx &a, const Fx &b) {
+  Fx r;
+  uint64_t c = 0;
+  for (int i = 0; i < 8; ++i) {
+    c += (uint64_t)a.w[i] + b.w[i];
+    r.w[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  return r;
+}
+CR_F Fx fx_negate(const Fx &a) {
+  Fx r;
+  uint64_t c = 1;
+  for (int i = 0; i < 8; ++i) {
+    c += (uint64_t)(~a.w[i]);
+    r.w[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  return r;
+}
+CR_F Fx fx_sub(const Fx &a, const Fx &b) { return fx_add(a, fx_negate(b)); }
+CR_F Fx fx_abs(const Fx &a) { return fx_neg_p(a) ? fx_negate(a) : a; }
+CR_F Fx fx_from_int(int64_t v) {
+  Fx r = fx_zero();
+  uint64_t m = v < 0 ? (uint64_t)(-v) : (uint64_t)v;
+  // integer part occupies bits 240..255: limb 7 bits 16..31
+  r.w[7] = (uint32_t)(m << 16);
+  return v < 0 ? fx_negate(r) : r;
+}
+// Exact conversion of a finite double with |v| < 2^15 and lsb >= 2^-240.
+CR_F Fx fx_from_double(double v) {
+  Fx r = fx_zero();
+  if (v == 0.0) return r;
+  uint64_t b = d2u(v);
+  int be = (int)((b >> 52) & 0x7FF);
+  uint64_t M = (b & 0xFFFFFFFFFFFFFull) | (be ? (1ull << 52) : 0);
+  int E = (be ? be : 1) - 1075;  // v = M * 2^E
+  int pos = E + FX_FRAC;         // bit index of M's lsb
+  if (pos < 0) {                 // truncate (never for the callers' inputs)
+    M = -pos >= 64 ? 0 : (M >> -pos);
+    pos = 0;
+  }
+  int limb = pos >> 5, sh = pos & 31;
+  uint64_t lo = M << sh;                       // bits 0..63 of the shifted M
+  uint64_t hi = sh ? (M >> (64 - sh)) : 0;    // bits 64..(52+sh)
+  if (limb < 8) r.w[limb] = (uint32_t)lo;
+  if (limb + 1 < 8) r.w[limb + 1] = (uint32_t)(lo >> 32);
+  if (limb + 2 < 8) r.w[limb + 2] = (uint32_t)hi;
+  return (b >> 63) ? fx_negate(r) : r;
+}
+// (a * b) >> 240 for non-negative a, b (truncating).
+CR_F Fx fx_mul(const Fx &a, const Fx &b) {
+  uint32_t p[16];
+  for (int i = 0; i < 16; ++i) p[i] = 0;
+  for (int i = 0; i < 8; ++i) {
+    uint64_t c = 0;
+    for (int j = 0; j < 8; ++j) {
+      uint64_t t = (uint64_t)a.w[i] * b.w[j] + p[i + j] + c;
+      p[i + j] = (uint32_t)t;
+      c = t >> 32;
+    }
+    p[i + 8] = (uint32_t)c;
+  }
+  // shift right by 240 = 7 limbs + 16 bits
+  Fx r;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t lo = p[i + 7], hi = (i + 8 < 16) ? p[i + 8] : 0;
+    r.w[i] = (lo >> 16) | (hi << 16);
+  }
+  return r;
+}
+// a * k for non-negative a and small k.
+CR_F Fx fx_mul_u32(const Fx &a, uint32_t k) {
+  Fx r;
+  uint64_t c = 0;
+  for (int i = 0; i < 8; ++i) {
+    c += (uint64_t)a.w[i] * k;
+    r.w[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  return r;
+}
+// a / d for non-negative a (truncating).
+CR_F Fx fx_div_u32(const Fx &a, uint32_t d) {
+  Fx r;
+  uint64_t rem = 0;
+  for (int i = 7; i >= 0; --i) {
+    uint64_t cur = (rem << 32) | a.w[i];
+    r.w[i] = (uint32_t)(cur / d);
+    rem = cur % d;
+  }
+  return r;
+}
+// 1/b for b in [1, 4) by Newton from the double reciprocal (3 steps: 53 -> 212+ bits).
+CR_F Fx fx_recip(const Fx &b, double bd) {
+  Fx r = fx_from_double(1.0 / bd);
+  Fx two = fx_from_int(2);
+  for (int it = 0; it < 3; ++it) r = fx_mul(r, fx_sub(two, fx_mul(b, r)));
+  return r;
+}
+CR_F Fx fx_ln2() {
+  // ln2 = 0.LN2_WORDS... ; value * 2^240 = top 240 fraction bits
+  Fx r;
+  // fraction bits f_1..f_240 -> limbs: bit (240 - j) holds f_j
+  // words[k] holds f_{32k+1} .. f_{32k+32}; shifting the 288-bit fraction
+  // right by 48 bits (288 - 240) gives the 240-bit integer.
+  uint32_t w[9];
+  for (int i = 0; i < 9; ++i) w[i] = LN2_WORDS[i];
+  // integer value = (w0 w1 ... w8) >> 48  (w0 most significant)
+  for (int i = 0; i < 8; ++i) {
+    // limb i (least significant first) = bits [32i, 32i+32) of (W >> 48)
+    // W's limb j (lsw first) = w[8 - j]
+    int j = i + 1;  // 48 = 32 + 16
+    uint32_t lo = (8 - j >= 0) ? w[8 - j] : 0;
+    uint32_t hi = (8 - j - 1 >= 0) ? w[8 - j - 1] : 0;
+    r.w[i] = (lo >> 16) | (hi << 16);
+  }
+  r.w[7] &= 0x0000FFFFu;  // integer part 0
+  return r;
+}
+
+// Exact rounding of v * 2^scale (v signed Fx) to binary64 in mode M. Sets
+// *undecided when the bits below the rounding point are within the Fx error
+// of a boundary (pattern 0x000.., 0x7FF.., 0x800.., 0xFFF.. over 64 bits).
+template <int M>
+CR_F double fx_round(const Fx &v, int scale, int *undecided) {
+  bool neg = fx_neg_p(v);
+  Fx a = fx_abs(v);
+  int top = -1;
+  for (int i = 7; i >= 0 && top < 0; --i)
+    if (a.w[i]) top = i * 32 + 31 - clz32(a.w[i]);
+  if (top < 0) return neg ? -0.0 : 0.0;
+  // value = a * 2^(scale - 240); leading bit weight 2^(top + scale - 240)
+  int ev = top + scale - FX_FRAC;
+  int prec = 53;
+  if (ev < -1022) prec = 53 - (-1022 - ev);
+  // bits: kept = a[top .. top-prec+1], rest below
+  auto bit_window64 = [&](int hi_bit) -> uint64_t {  // 64 bits a[hi_bit .. hi_bit-63]
+    uint64_t r = 0;
+    for (int k = 0; k < 64; ++k) {
+      int b = hi_bit - k;
+      uint64_t bit = (b >= 0 && b < 256) ? ((a.w[b >> 5] >> (b & 31)) & 1u) : 0;
+      r = (r << 1) | bit;
+    }
+    return r;
+  };
+  uint64_t kept = 0;
+  if (prec > 0) kept = bit_window64(top) >> (64 - prec);
+  int rest_top = top - (prec > 0 ? prec : 0);  // first bit below kept
+  if (prec <= 0) rest_top = top - prec;        // leading bits are below half of min subnormal
+  uint64_t R = bit_window64(rest_top);          // 64 bits just below the rounding point
+  bool sticky_below = false;
+  for (int b = rest_top - 64; b >= 0 && !sticky_below; --b)
+    if ((a.w[b >> 5] >> (b & 31)) & 1u) sticky_below = true;
+  if (prec <= 0) {
+    // value < 2^-1074 (prec==0: in [2^-1075, 2^-1074)); R holds bits from
+    // weight 2^-1075 downward (with leading zeros when prec < 0).
+    kept = 0;
+  }
+  if (R == 0 || R == ~0ull || R == 0x8000000000000000ull || R == 0x7FFFFFFFFFFFFFFFull)
+    *undecided = 1;
+  bool round_bit = (R >> 63) & 1;
+  bool inexact = R != 0 || sticky_below;
+  bool up;
+  if (M == RNE) up = round_bit && ((R << 1) != 0 || sticky_below || (kept & 1));
+  else if (M == RZ) up = false;
+  else if (M == RU) up = !neg && inexact;
+  else up = neg && inexact;
+  int e = ev;
+  int p = prec > 0 ? prec : 0;
+  if (up) {
+    kept += 1;
+    if (ev >= -1022 && (kept >> p)) {  // carry out of a normal significand
+      kept >>= 1;
+      e += 1;
+    }
+    if (p == 0) {  // rounded up to the min subnormal
+      return neg ? -0x1p-1074 : 0x1p-1074;
+    }
+  }
+  if (p == 0) return neg ? -0.0 : 0.0;
+  if (e > 1023) {
+    bool inf = M == RNE || (M == RU && !neg) || (M == RD && neg);
+    return inf ? (neg ? -INFINITY : INFINITY) : (neg ? -0x1.fffffffffffffp1023 : 0x1.fffffffffffffp1023);
+  }
+  uint64_t bits;
+  if (ev < -1022) {
+    // subnormal: kept is the significand at 2^-1074 granularity (may have
+    // carried into the normal range, which the encoding handles naturally)
+    bits = kept;
+  } else {
+    bits = ((uint64_t)(e + 1023) << 52) | (kept & 0xFFFFFFFFFFFFFull);
+  }
+  return u2d(bits | (neg ? 0x8000000000000000ull : 0));
+}
+
+// ------------------------------------------------------- exp2 accurate ----
+// 2^x = 2^N * e^(f ln2), N = floor(x), f in [0,1) exact in Fx; e^y by Taylor.
+template <int M>
+CR_F double exp2d_accurate(double x, int *undecided) {
+  double N = floor(x);
+  Fx f = fx_sub(fx_from_double(x), fx_from_int((int64_t)N));
+  Fx y = fx_mul(f, fx_ln2());
+  Fx sum = fx_from_int(1), term = fx_from_int(1);
+  for (uint32_t n = 1; n < 80; ++n) {
+    term = fx_div_u32(fx_mul(term, y), n);
+    if (fx_is_zero(term)) break;
+    sum = fx_add(sum, term);
+  }
+  return fx_round<M>(sum, (int)N, undecided);
+}
+
+// -------------------------------------------------------- log accurate ----
+// log x = e ln2 + 2 atanh((m-1)/(m+1)), m in [0.75, 1.5).
+template <int M>
+CR_F double logd_accurate(double x, int *undecided) {
+  int eadj = 0;
+  if (x < 0x1p-1022) {
+    x *= 0x1p54;
+    eadj = -54;
+  }
+  int h = d2hi(x);
+  int hh = h - 0x3FE80000;
+  int e = (hh >> 20) + eadj;
+  double m = hilo2d(h - ((hh >> 20) << 20), d2lo(x));
+  Fx mf = fx_from_double(m);
+  Fx one = fx_from_int(1);
+  Fx num = fx_sub(mf, one);
+  Fx den = fx_add(mf, one);
+  bool sneg = fx_neg_p(num);
+  Fx s = fx_mul(fx_abs(num), fx_recip(den, m + 1.0));
+  Fx s2 = fx_mul(s, s);
+  Fx sum = s, t = s;
+  for (uint32_t k = 1; k < 80; ++k) {
+    t = fx_mul(t, s2);
+    if (fx_is_zero(t)) break;
+    sum = fx_add(sum, fx_div_u32(t, 2 * k + 1));
+  }
+  sum = fx_add(sum, sum);  // 2 atanh(s) = |log m|
+  if (sneg) sum = fx_negate(sum);
+  Fx el = fx_mul_u32(fx_ln2(), (uint32_t)(e < 0 ? -e : e));
+  if (e < 0) el = fx_negate(el);
+  return fx_round<M>(fx_add(el, sum), 0, undecided);
+}
+
+// --------------------------------------------------------- fast paths ----
+struct F64Tab {
+  double t1h[16], t1l[16], t2h[16], t2l[16], t3h[16], t3l[16];
+  double lc[128], llh[128], lll[128];
+};
+
+struct F64Out {
+  double y;
+  bool decided;
+};
+
+// Round test (ref: proj/src/kernels_f64.cpp:63-76) for a normalized DD
+// v = h + l (|l| <= ulp(h)/2) with absolute error bound b.
+template <int M>
+CR_F F64Out round_test64(double h, double l, double b) {
+  uint64_t hb = d2u(h);
+  int eh = (int)((hb >> 52) & 0x7FF);
+  bool pow2 = (hb & 0xFFFFFFFFFFFFFull) == 0;
+  double half_ulp = u2d((uint64_t)(eh - 53 > 0 ? eh - 53 : 1) << 52);  // 2^(exp(h)-53)
+  double al = dabs(l);
+  if (M == RNE) {
+    double lim = (pow2 && ((l < 0) != (h < 0))) ? half_ulp * 0.5 : half_ulp;
+    return {h, add_(al, b) < lim};
+  }
+  bool dec = al > b;
+  bool lpos = l > 0, hpos = h > 0;
+  uint64_t r = hb;
+  if (M == RZ) {
+    if (lpos != hpos) r = hb - 1;
+  } else if (M == RU) {
+    if (lpos) r = hpos ? hb + 1 : hb - 1;
+  } else {
+    if (!lpos) r = hpos ? hb - 1 : hb + 1;
+  }
+  return {u2d(r), dec};
+}
+
+constexpr double EPS_EXP2D = 0x1p-74;
+constexpr double EPS_LOGD = 0x1p-73;
+
+template <int M>
+CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
+  uint64_t xb = d2u(x);
+  if (x != x) return {u2d(xb | 0x0008000000000000ull), true};
+  if (x == INFINITY) return {INFINITY, true};
+  if (x >= 1024.0) {
+    bool inf = M == RNE || M == RU;
+    return {inf ? INFINITY : 0x1.fffffffffffffp1023, true};
+  }
+  if (x <= -1075.0) {  // 2^x <= 2^-1075 (tie at -1075 rounds to even = 0)
+    return {M == RU && x != -INFINITY ? 0x1p-1074 : 0.0, true};
+  }
+  if (x == floor(x)) {  // exact power of two in [-1074, 1023]
+    int n = (int)x;
+    double p = n >= -1022 ? u2d((uint64_t)(n + 1023) << 52) : u2d(1ull << (n + 1074));
+    return {p, true};
+  }
+  if (dabs(x) <= 0x1p-55) {
+    if (x > 0) return {M == RU ? 1.0 + 0x1p-52 : 1.0, true};
+    return {(M == RZ || M == RD) ? 1.0 - 0x1p-53 : 1.0, true};
+  }
+  double t = fma_(x, 4096.0, SHIFTER);
+  double kd = sub_(t, SHIFTER);
+  int k = (int)d2lo(t);
+  double R = fma_(kd, -0x1p-12, x);  // exact, |R| <= 2^-13
+  int N = k >> 12, i1 = (k >> 8) & 15, i2 = (k >> 4) & 15, i3 = k & 15;
+  DD Tv = dd_mul(dd_mul(DD{T.t1h[i1], T.t1l[i1]}, DD{T.t2h[i2], T.t2l[i2]}), DD{T.t3h[i3], T.t3l[i3]});
+  double q = fma_(fma_(fma_(fma_(EXP2D_Q[5], R, EXP2D_Q[4]), R, EXP2D_Q[3]), R, EXP2D_Q[2]), R,
+                  EXP2D_Q[1]);
+  q = fma_(q, R, EXP2D_Q[0]);
+  DD lin = two_prod(R, LN2D_H);
+  DD s = fast_two_sum(1.0, lin.hi);
+  double lo = add_(add_(s.lo, lin.lo), fma_(R, LN2D_L, mul_(mul_(R, R), q)));
+  DD P = fast_two_sum(s.hi, lo);
+  DD V = dd_mul(Tv, P);
+  V = fast_two_sum(V.hi, V.lo);
+  F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
+  if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
+  // scale by 2^N (exact for normal results; 2^1024 overflow only when rounding to 2)
+  r.y = mul_(mul_(r.y, u2d((uint64_t)((N >> 1) + 1023) << 52)),
+             u2d((uint64_t)((N - (N >> 1)) + 1023) << 52));
+  return r;
+}
+
+template <int M>
+CR_F F64Out logd_fast(double x, const F64Tab &T) {
+  uint64_t xb = d2u(x);
+  if (x != x) return {u2d(xb | 0x0008000000000000ull), true};
+  if (x == 0.0) return {-INFINITY, true};
+  if (xb >> 63) return {u2d(0x7FF8000000000000ull), true};
+  if (x == INFINITY) return {INFINITY, true};
+  if (x == 1.0) return {0.0, true};
+  int eadj = 0;
+  double xs = x;
+  if (x < 0x1p-1022) {
+    xs = x * 0x1p54;
+    eadj = -54;
+  }
+  int h = d2hi(xs);
+  int hh = h - 0x3FE80000;
+  int e = (hh >> 20) + eadj;
+  int i = (hh >> 13) & 127;
+  double m = hilo2d(h - ((hh >> 20) << 20), d2lo(xs));
+  double c = T.lc[i];
+  DD pm = two_prod(m, c);
+  DD r = fast_two_sum(sub_(pm.hi, 1.0), pm.lo);  // r = m c - 1 exactly
+  double rh = r.hi, rl = r.lo;
+  DD sq = two_prod(rh, rh);
+  DD b = {-0.5 * sq.hi, -0.5 * sq.lo};             // -rh^2/2 (exact)
+  DD cube = dd_mul_d(sq, rh);                       // rh^3
+  DD c3 = dd_mul(cube, DD{THIRD_H, THIRD_L});       // rh^3/3
+  double qt = LOGD_TAIL[8];
+  for (int n = 7; n >= 0; --n) qt = fma_(qt, rh, LOGD_TAIL[n]);
+  double rest = mul_(mul_(sq.hi, sq.hi), qt);       // rh^4 (-1/4 + rh/5 - ...)
+  double corr = mul_(rl, fma_(rh, sub_(rh, 1.0), 1.0));  // rl (1 - rh + rh^2)
+  DD u = fast_two_sum(rh, b.hi);
+  double small = add_(add_(add_(add_(u.lo, b.lo), c3.hi), add_(rest, corr)), c3.lo);
+  DD P = fast_two_sum(u.hi, small);
+  double ed = i2d(e);
+  DD el = two_sum(mul_(ed, LN2_H), mul_(ed, LN2_M));
+  el = dd_add_d(el, mul_(ed, LN2_L));
+  DD V = dd_add(dd_add(el, DD{T.llh[i], T.lll[i]}), P);
+  return round_test64<M>(V.hi, V.lo, EPS_LOGD * dabs(V.hi));
+}
+
+}  // namespace crvec

@@ -1,0 +1,49 @@
+// DEVELOPER TOOL ONLY: g++ build of the binary64 device math for CPU debugging.
+#define CRVEC_EMU 1
+#include <cstdint>
+#include <cstring>
+#include "../../paper_2605_15547_b200/csrc/crvec_fns_f64.cuh"
+using namespace crvec;
+static F64Tab T;
+static void init() {
+  static bool done = false;
+  if (done) return;
+  std::memcpy(T.t1h, EXP2D_T1_HI, 128); std::memcpy(T.t1l, EXP2D_T1_LO, 128);
+  std::memcpy(T.t2h, EXP2D_T2_HI, 128); std::memcpy(T.t2l, EXP2D_T2_LO, 128);
+  std::memcpy(T.t3h, EXP2D_T3_HI, 128); std::memcpy(T.t3l, EXP2D_T3_LO, 128);
+  std::memcpy(T.lc, LOGD_C, 1024); std::memcpy(T.llh, LOGD_L_HI, 1024); std::memcpy(T.lll, LOGD_L_LO, 1024);
+  done = true;
+}
+template <int M>
+static double one(int fn, double x, int force, uint64_t *st) {
+  F64Out r = fn == 0 ? exp2d_fast<M>(x, T) : logd_fast<M>(x, T);
+  if (!r.decided || (force && !(x != x) && r.decided == true && force == 2)) {
+    ++st[0];
+    int und = 0;
+    r.y = fn == 0 ? exp2d_accurate<M>(x, &und) : logd_accurate<M>(x, &und);
+    st[1] += und;
+  }
+  return r.y;
+}
+extern "C" int emu64(int fn, const double *x, double *y, uint64_t n, int force, uint64_t *st) {
+  init();
+  for (uint64_t i = 0; i < n; ++i) {
+    y[4 * i + 0] = one<RNE>(fn, x[i], force, st);
+    y[4 * i + 1] = one<RZ>(fn, x[i], force, st);
+    y[4 * i + 2] = one<RU>(fn, x[i], force, st);
+    y[4 * i + 3] = one<RD>(fn, x[i], force, st);
+  }
+  return 0;
+}
+// accurate path only (for testing it directly on arbitrary inputs)
+extern "C" int emu64_acc(int fn, const double *x, double *y, uint64_t n, uint64_t *st) {
+  for (uint64_t i = 0; i < n; ++i) {
+    int u = 0;
+    y[4 * i + 0] = fn == 0 ? exp2d_accurate<RNE>(x[i], &u) : logd_accurate<RNE>(x[i], &u);
+    y[4 * i + 1] = fn == 0 ? exp2d_accurate<RZ>(x[i], &u) : logd_accurate<RZ>(x[i], &u);
+    y[4 * i + 2] = fn == 0 ? exp2d_accurate<RU>(x[i], &u) : logd_accurate<RU>(x[i], &u);
+    y[4 * i + 3] = fn == 0 ? exp2d_accurate<RD>(x[i], &u) : logd_accurate<RD>(x[i], &u);
+    st[1] += u;
+  }
+  return 0;
+}

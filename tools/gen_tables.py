@@ -284,6 +284,52 @@ def gen_atrig():
     arr("ATANT_HI", [dd(v)[0] for v in an]); arr("ATANT_LO", [dd(v)[1] for v in an])
 
 
+# ---------------------------------------------------------------- binary64 --
+def gen_f64():
+    """Tables for the binary64 exp2 / log fast paths (ref: PAPER.md II.B;
+    ref: proj/include/crvec/tables.hpp:33-51) and the multiword constants of
+    their accurate path."""
+    emit("// ---- binary64 exp2: x = N + (i1*256 + i2*16 + i3)/4096 + R, three DD tables ----")
+    for lvl, den in ((1, 16), (2, 256), (3, 4096)):
+        T = [mp.mpf(2) ** (mp.mpf(j) / den) for j in range(16)]
+        arr(f"EXP2D_T{lvl}_HI", [dd(t)[0] for t in T])
+        arr(f"EXP2D_T{lvl}_LO", [dd(t)[1] for t in T])
+    # 2^R = 1 + R ln2 + R^2 q(R), q Taylor (|R ln2| <= 2^-13.5, truncation < 2^-106)
+    q = [LN2 ** n / mp.factorial(n) for n in range(2, 8)]
+    arr("EXP2D_Q", [d(c) for c in q])
+    h, l = dd(LN2)
+    scalar("LN2D_H", h); scalar("LN2D_L", l)
+    emit("// ---- binary64 log: m in [0.75, 1.5), 128 bins, c_i = 1/mid (7 bits) ----")
+    cs, Ls = [], []
+    for i in range(128):
+        if i < 64:
+            a = mp.mpf("0.75") + mp.mpf(i) / 256
+            b = a + mp.mpf(1) / 256
+        else:
+            a = 1 + mp.mpf(i - 64) / 128
+            b = a + mp.mpf(1) / 128
+        c = mp.mpf(1) if i in (63, 64) else mp.mpf(trunc_bits(2 / (a + b), 7))
+        cs.append(float(c))
+        Ls.append(-mp.log(c))
+    arr("LOGD_C", cs)
+    arr("LOGD_L_HI", [dd(v)[0] for v in Ls])
+    arr("LOGD_L_LO", [dd(v)[1] for v in Ls])
+    arr("LOGD_TAIL", [d(mp.mpf((-1) ** (n + 1)) / n) for n in range(4, 13)])
+    h, l = dd(mp.mpf(1) / 3)
+    scalar("THIRD_H", h); scalar("THIRD_L", l)
+    # multiword: ln2 to 288 bits as 9 x u32, most significant first (value = 0.w0 w1 ...)
+    v = LN2
+    words = []
+    for _ in range(9):
+        v *= mp.mpf(2) ** 32
+        w = int(mp.floor(v))
+        words.append(w)
+        v -= w
+    emit("static CR_CONST unsigned LN2_WORDS[9] = {")
+    emit("    " + ", ".join(f"0x{w:08x}u" for w in words) + ",")
+    emit("};")
+
+
 def generate():
     lines.clear()
     report.clear()
@@ -293,6 +339,7 @@ def generate():
     gen_log()
     gen_trig()
     gen_atrig()
+    gen_f64()
     return "\n".join(lines) + "\n"
 
 
