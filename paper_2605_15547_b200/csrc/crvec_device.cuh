@@ -215,24 +215,28 @@ CR_F uint32_t round_dd(double h, double l) {
   return f2u(cvt_f32<M>(u2d(b)));
 }
 
-// One fast-path result.
+// One fast-path result: `a` approximates f(x) with relative error below
+// E * 2^-53 whenever `main` is set. Lanes outside the function's main range
+// (IEEE specials, tiny-argument and saturation rules) are resolved by the
+// function's special<M>() in a rare, warp-uniform branch, so the common path
+// carries only one range check.
 struct Fast {
-  double a;   // approximation of f(x) (or the exact value when skip)
-  bool skip;  // a is exact / already decided: no rounding test
+  double a;
+  bool main;
 };
 
-// Final assembly of a fast-path lane: static-mode conversion, invalid and
-// NaN-payload policy of ref: proj/src/kernels_f32.cpp:52,111-115 by integer
-// select (quiet(x): payload and sign kept; invalid: +qNaN 0x7FC00000).
+// Common-path assembly: one static-mode conversion and the rounding test.
 template <int M>
-CR_F uint32_t finish(uint32_t xb, Fast r, bool &fail, uint32_t E) {
-  uint32_t y = f2u(cvt_f32<M>(r.a));
-  if (r.a != r.a) y = 0x7FC00000u;
-  bool xnan = (xb & 0x7FFFFFFFu) > 0x7F800000u;
-  if (xnan) y = xb | 0x00400000u;
-  fail = !r.skip && !xnan && near_boundary(r.a, E);
-  return y;
+CR_F uint32_t finish(Fast r, bool &fail, uint32_t E) {
+  fail = r.main && near_boundary(r.a, E);
+  return f2u(cvt_f32<M>(r.a));
 }
+
+// lo <= u < hi (unsigned), one subtract + one compare.
+CR_F bool in_range(uint32_t u, uint32_t lo, uint32_t hi) { return u - lo < hi - lo; }
+CR_F bool nan_bits(uint32_t xb) { return (xb << 1) > 0xFF000000u; }
+// quiet(x): payload and sign kept (ref: proj/include/crvec/fpbits.hpp:101-102).
+CR_F uint32_t quiet_bits(uint32_t xb) { return xb | 0x00400000u; }
 
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);
 // valid while the result stays normal.

@@ -21,16 +21,20 @@ namespace crvec {
 
 // Polynomials (Horner, coefficients from tools/gen_tables.py).
 CR_F double expq(double r) {
-  return fma_(fma_(fma_(fma_(EXPQ_C4, r, EXPQ_C3), r, EXPQ_C2), r, EXPQ_C1), r, EXPQ_C0);
+  return fma_(fma_(fma_(fma_(EXPQ[4], r, EXPQ[3]), r, EXPQ[2]), r, EXPQ[1]), r, EXPQ[0]);
 }
 CR_F double logq(double r) {
-  double q = fma_(LOGQ_C7, r, LOGQ_C6);
-  q = fma_(q, r, LOGQ_C5);
-  q = fma_(q, r, LOGQ_C4);
-  q = fma_(q, r, LOGQ_C3);
-  q = fma_(q, r, LOGQ_C2);
-  q = fma_(q, r, LOGQ_C1);
-  return fma_(q, r, LOGQ_C0);
+  double q = fma_(LOGQ[6], r, LOGQ[5]);
+  q = fma_(q, r, LOGQ[4]);
+  q = fma_(q, r, LOGQ[3]);
+  q = fma_(q, r, LOGQ[2]);
+  q = fma_(q, r, LOGQ[1]);
+  return fma_(q, r, LOGQ[0]);
+}
+
+// Copy the sign of binary32 bits xb onto a double (integer op on the high word).
+CR_F double with_sign(double a, uint32_t xb) {
+  return hilo2d(d2hi(a) ^ (int)(xb & 0x80000000u), d2lo(a));
 }
 
 // ============================================================ exp family ====
@@ -39,6 +43,25 @@ CR_F double exp_core(int k, double r, double tab) {
   double T = CR_TAB(tab, EXP2J_HI, k & 15);
   double p = fma_(mul_(r, r), expq(r), r);  // e^r - 1
   return scale2(fma_(T, p, T), k >> 4);
+}
+
+// Cubic-Q variant (2^-40.1 relative on e^r - 1, i.e. < 2^-45.5 on the
+// result): the rounding-test tolerance E = 512 covers it with margin.
+CR_F double expq3(double r) { return fma_(fma_(fma_(EXPQ3[3], r, EXPQ3[2]), r, EXPQ3[1]), r, EXPQ3[0]); }
+CR_F double exp_core3(int k, double r, double tab) {
+  double T = CR_TAB(tab, EXP2J_HI, k & 15);
+  double p = fma_(mul_(r, r), expq3(r), r);  // e^r - 1
+  return scale2(fma_(T, p, T), k >> 4);
+}
+// Non-main lanes of exp / exp2 / exp10: NaN, +-0 -> 1, +Inf -> +Inf,
+// -Inf -> +0, tiny |x|: b^x lies in the gap beside 1 (above for x > 0).
+template <int M>
+CR_F uint32_t exp_like_special(uint32_t xb) {
+  uint32_t az = xb << 1;
+  if (nan_bits(xb)) return quiet_bits(xb);
+  if (az == 0) return 0x3F800000u;
+  if (az == 0xFF000000u) return (int)xb < 0 ? 0u : 0x7F800000u;
+  return f2u(cvt_f32<M>((int)xb > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31));
 }
 
 // Double-double e^r, |r| <= ln2/32: Taylor to r^13 (error < 2^-104).
@@ -77,21 +100,16 @@ CR_F DD red_exp_dd(double xc, int &k) {
 }
 
 struct FnExp {
-  static constexpr uint32_t E = 8;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    double xc = fmin(fmax(xd, -104.5), 89.5);
-    RedExp q = red_exp(xc);
-    double a = exp_core(q.k, q.r, R.t);
-    bool skip = false;
-    if (dabs(xd) <= 0x1p-26) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
-    if (xd == 0.0) { a = 1.0; skip = true; }
-    if (x == INFINITY) { a = INFINITY; skip = true; }
-    if (x == -INFINITY) { a = 0.0; skip = true; }
-    return {a, skip};
+    RedExp q = red_exp(f2d(fminf(fmaxf(x, -104.5f), 89.5f)));
+    // main: 2^-26 < |x| < inf (saturation is handled by the clamp)
+    return Fast{exp_core3(q.k, q.r, R.t), in_range(f2u(x) << 1, 0x65000002u, 0xFF000000u)};
   }
+  template <int M>
+  CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
     double xc = fmin(fmax(f2d(x), -104.5), 89.5);
     int k;
@@ -101,24 +119,21 @@ struct FnExp {
 };
 
 struct FnExp2 {
-  static constexpr uint32_t E = 8;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    double xc = fmin(fmax(xd, -151.5), 129.5);
+    double xc = f2d(fminf(fmaxf(x, -151.5f), 129.5f));
     double t = fma_(xc, 16.0, SHIFTER);
     double kd = sub_(t, SHIFTER);
     double u = fma_(kd, -0.0625, xc);  // exact
-    int k = (int)d2lo(t);
-    double a = exp_core(k, mul_(u, LN2_D), R.t);
-    bool skip = (u == 0.0) && ((k & 15) == 0);  // 2^integer: exact
-    if (dabs(xd) <= 0x1p-26) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
-    if (xd == 0.0) { a = 1.0; skip = true; }
-    if (x == INFINITY) { a = INFINITY; skip = true; }
-    if (x == -INFINITY) { a = 0.0; skip = true; }
-    return {a, skip};
+    // integer x gives 2^x exactly: the rounding test sends it to the accurate
+    // path, whose exact-value snap returns it in every mode.
+    return Fast{exp_core3((int)d2lo(t), mul_(u, LN2_D), R.t),
+                in_range(f2u(x) << 1, 0x65000002u, 0xFF000000u)};
   }
+  template <int M>
+  CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
     double xc = fmin(fmax(f2d(x), -151.5), 129.5);
     double t = fma_(xc, 16.0, SHIFTER);
@@ -131,26 +146,21 @@ struct FnExp2 {
 };
 
 struct FnExp10 {
-  static constexpr uint32_t E = 8;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    double xc = fmin(fmax(xd, -45.5), 39.5);
+    double xc = f2d(fminf(fmaxf(x, -45.5f), 39.5f));
     double t = fma_(xc, LOG2_10_16, SHIFTER);
     double kd = sub_(t, SHIFTER);
     double r = fma_(xc, LN10_H, -mul_(kd, LN2_16_H));
     r = fma_(xc, LN10_M, r);
     r = fma_(kd, -LN2_16_M, r);
     r = fma_(xc, LN10_L, r);
-    double a = exp_core((int)d2lo(t), r, R.t);
-    bool skip = false;
-    if (dabs(xd) <= 0x1p-28) { a = xd > 0 ? 1.0 + 0x1p-30 : 1.0 - 0x1p-31; skip = true; }
-    if (xd == 0.0) { a = 1.0; skip = true; }
-    if (x == INFINITY) { a = INFINITY; skip = true; }
-    if (x == -INFINITY) { a = 0.0; skip = true; }
-    return {a, skip};
+    return Fast{exp_core3((int)d2lo(t), r, R.t), in_range(f2u(x) << 1, 0x63000002u, 0xFF000000u)};
   }
+  template <int M>
+  CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
     double xc = fmin(fmax(f2d(x), -45.5), 39.5);
     double t = fma_(xc, LOG2_10_16, SHIFTER);
@@ -166,28 +176,32 @@ struct FnExp10 {
 };
 
 struct FnExpm1 {
-  static constexpr uint32_t E = 16;
+  static constexpr uint32_t E = 32;
   struct Regs { double t, tl; };
   CR_F static void load(Regs &R) {
     R.t = CR_TAB_LOAD(EXP2J_HI);
     R.tl = CR_TAB_LOAD(EXP2J_LO);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    double xc = fmin(fmax(xd, -18.5), 89.5);
-    RedExp q = red_exp(xc);
+    uint32_t xb = f2u(x);
+    RedExp q = red_exp(f2d(fminf(fmaxf(x, -18.5f), 89.5f)));
     int j = q.k & 15, e = q.k >> 4;
     double T = scale2(CR_TAB(R.t, EXP2J_HI, j), e);
     double Tl = CR_TAB(R.tl, EXP2J_LO, j) * scale2(1.0, e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
-    double a = fma_(T, p, add_(sub_(T, 1.0), Tl));
-    bool skip = false;
-    if (xd < -18.0) { a = -1.0 + 0x1p-40; skip = true; }
-    if (dabs(xd) <= 0x1p-26) { a = fma_(dabs(xd), 0x1p-36, xd); skip = true; }
-    if (xd == 0.0) { a = xd; skip = true; }
-    if (x == INFINITY) { a = INFINITY; skip = true; }
-    if (x == -INFINITY) { a = -1.0; skip = true; }
-    return {a, skip};
+    // main: 2^-26 < |x| < inf and x >= -18
+    return Fast{fma_(T, p, add_(sub_(T, 1.0), Tl)),
+                in_range(xb << 1, 0x65000002u, 0xFF000000u) && xb <= 0xC1900000u};
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0) return xb;
+    if (az == 0xFF000000u) return (int)xb < 0 ? 0xBF800000u : 0x7F800000u;
+    double xd = f2d(x);
+    if (x < -18.0f) return f2u(cvt_f32<M>(-1.0 + 0x1p-40));  // (-1, -1 + 2^-25)
+    return f2u(cvt_f32<M>(fma_(dabs(xd), 0x1p-36, xd)));     // x + x^2/2 beside x
   }
   CR_F static DD slow(float x) {
     double xc = fmin(fmax(f2d(x), -18.5), 89.5);
@@ -214,8 +228,8 @@ CR_F HypParts hyp_parts(double ax, double tab, double tabl) {
   double Ep = CR_TAB(tab, EXP2J_HI, kp & 15) * s1, Elp = CR_TAB(tabl, EXP2J_LO, kp & 15) * s1;
   double Em = CR_TAB(tab, EXP2J_HI, km & 15) * s2, Elm = CR_TAB(tabl, EXP2J_LO, km & 15) * s2;
   double s = mul_(q.r, q.r);
-  double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ_C2, s, SINHQ_C1), s, SINHQ_C0), q.r);
-  double cr = fma_(s, fma_(fma_(COSHQ_C2, s, COSHQ_C1), s, COSHQ_C0), 1.0);
+  double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ[2], s, SINHQ[1]), s, SINHQ[0]), q.r);
+  double cr = fma_(s, fma_(fma_(COSHQ[2], s, COSHQ[1]), s, COSHQ[0]), 1.0);
   double Sa = mul_(add_(sub_(Ep, Em), sub_(Elp, Elm)), 0.5);
   double Ca = mul_(add_(Ep, Em), 0.5);
   return {Sa, Ca, sr, cr};
@@ -252,14 +266,18 @@ struct FnSinh {
     R.tl = CR_TAB_LOAD(EXP2J_LO);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x), ax = fmin(dabs(xd), 90.0);
-    HypParts h = hyp_parts(ax, R.t, R.tl);
-    double a = fma_(h.Sa, h.cr, mul_(h.Ca, h.sr));
-    a = xd < 0 ? -a : a;
-    bool skip = false;
-    if (dabs(xd) <= 0x1p-12) { a = fma_(xd, 0x1p-36, xd); skip = true; }
-    if (xd == 0.0 || dabs(xd) == INFINITY) { a = xd; skip = true; }
-    return {a, skip};
+    uint32_t xb = f2u(x);
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t, R.tl);
+    return Fast{with_sign(fma_(h.Sa, h.cr, mul_(h.Ca, h.sr)), xb),
+                in_range(xb << 1, 0x73000002u, 0xFF000000u)};  // 2^-12 < |x| < inf
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0 || az == 0xFF000000u) return xb;
+    double xd = f2d(x);
+    return f2u(cvt_f32<M>(fma_(xd, 0x1p-36, xd)));  // x + x^3/6 just above |x|
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);
@@ -277,14 +295,17 @@ struct FnCosh {
     R.tl = CR_TAB_LOAD(EXP2J_LO);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x), ax = fmin(dabs(xd), 90.0);
-    HypParts h = hyp_parts(ax, R.t, R.tl);
-    double a = fma_(h.Ca, h.cr, mul_(h.Sa, h.sr));
-    bool skip = false;
-    if (dabs(xd) <= 0x1p-13) { a = 1.0 + 0x1p-30; skip = true; }
-    if (xd == 0.0) { a = 1.0; skip = true; }
-    if (dabs(xd) == INFINITY) { a = INFINITY; skip = true; }
-    return {a, skip};
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t, R.tl);
+    return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)),
+                in_range(f2u(x) << 1, 0x72000002u, 0xFF000000u)};  // 2^-13 < |x| < inf
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0) return 0x3F800000u;
+    if (az == 0xFF000000u) return 0x7F800000u;
+    return f2u(cvt_f32<M>(1.0 + 0x1p-30));  // 1 + x^2/2 in (1, 1 + 2^-24)
   }
   CR_F static DD slow(float x) {
     HypDD h = hyp_parts_dd(fmin(dabs(f2d(x)), 90.0));
@@ -300,18 +321,22 @@ struct FnTanh {
     R.tl = CR_TAB_LOAD(EXP2J_LO);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x), ax = fmin(dabs(xd), 10.0);
-    HypParts h = hyp_parts(ax, R.t, R.tl);
+    uint32_t xb = f2u(x);
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 10.0f)), R.t, R.tl);
     double sh = fma_(h.Sa, h.cr, mul_(h.Ca, h.sr));
     double ch = fma_(h.Ca, h.cr, mul_(h.Sa, h.sr));
-    double a = div_fast(sh, ch);
-    a = xd < 0 ? -a : a;
-    bool skip = false;
-    if (dabs(xd) >= 10.0) { a = xd > 0 ? 1.0 - 0x1p-40 : -1.0 + 0x1p-40; skip = true; }
-    if (dabs(xd) <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
-    if (xd == 0.0) { a = xd; skip = true; }
-    if (dabs(xd) == INFINITY) { a = xd > 0 ? 1.0 : -1.0; skip = true; }
-    return {a, skip};
+    return Fast{with_sign(div_fast(sh, ch), xb),
+                in_range(xb << 1, 0x73000002u, 0x82400000u)};  // 2^-12 < |x| < 10
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0) return xb;
+    if (az == 0xFF000000u) return (int)xb < 0 ? 0xBF800000u : 0x3F800000u;
+    double xd = f2d(x);
+    if (az >= 0x82400000u) return f2u(cvt_f32<M>(with_sign(1.0 - 0x1p-40, xb)));  // |x| >= 10
+    return f2u(cvt_f32<M>(fma_(-xd, 0x1p-36, xd)));  // x - x^3/3 just below |x|
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);
@@ -340,31 +365,35 @@ CR_F RedLog red_log(double xd) {
 
 template <int BASE>  // 0: ln, 2: log2, 10: log10
 struct FnLogB {
-  static constexpr uint32_t E = 8;
-  struct Regs { float c; double l; };
+  static constexpr uint32_t E = 32;
+  struct Regs { int c; double l; };
   CR_F static void load(Regs &R) {
-    R.c = CR_TAB_LOAD(LOG_C);
+    R.c = CR_TAB_LOAD(LOG_C_HI);
     R.l = BASE == 0 ? CR_TAB_LOAD(LOG_L_HI) : BASE == 2 ? CR_TAB_LOAD(LOG2_L_HI) : CR_TAB_LOAD(LOG10_L_HI);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    RedLog q = red_log(xd);
-    double c = f2d(CR_TAB(R.c, LOG_C, q.i));
+    uint32_t xb = f2u(x);
+    RedLog q = red_log(f2d(x));
+    double c = hilo2d(CR_TAB(R.c, LOG_C_HI, q.i), 0u);  // c_i has <= 21 significant bits
     double L = BASE == 0 ? CR_TAB(R.l, LOG_L_HI, q.i)
                          : BASE == 2 ? CR_TAB(R.l, LOG2_L_HI, q.i) : CR_TAB(R.l, LOG10_L_HI, q.i);
-    double r = fma_(q.m, c, -1.0);
+    double r = fma_(q.m, c, -1.0);  // exact
     double p = fma_(mul_(r, r), logq(r), r);
     double ed = i2d(q.e), a;
     if (BASE == 0) a = add_(fma_(ed, LN2_D, L), p);
     else if (BASE == 2) a = fma_(p, INV_LN2, add_(ed, L));
     else a = fma_(p, INV_LN10, fma_(ed, LOG10_2, L));
-    bool skip = false;
+    // main: 0 < x < +Inf. Exact results (x = 1, 2^k, 10^k) fail the rounding
+    // test and are returned exactly by the accurate path's snap.
+    return Fast{a, xb - 1u < 0x7F7FFFFFu};
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
-    if (xb == 0x3F800000u) { a = 0.0; skip = true; }
-    if ((xb & 0x7FFFFFFFu) == 0) { a = -INFINITY; skip = true; }
-    if (xb > 0x80000000u) { a = NAN; skip = true; }
-    if (xb == 0x7F800000u) { a = INFINITY; skip = true; }
-    return {a, skip};
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if ((xb << 1) == 0) return 0xFF800000u;
+    if (xb == 0x7F800000u) return 0x7F800000u;
+    return 0x7FC00000u;  // x < 0
   }
   CR_F static DD log_dd_core(int e, int i, DD r) {
     // log1p(r) = sum_{n=1}^{24} (-1)^(n+1) r^n / n
@@ -388,28 +417,34 @@ using FnLog2 = FnLogB<2>;
 using FnLog10 = FnLogB<10>;
 
 struct FnLog1p {
-  static constexpr uint32_t E = 8;
-  struct Regs { float c; double l; };
+  static constexpr uint32_t E = 32;
+  struct Regs { int c; double l; };
   CR_F static void load(Regs &R) {
-    R.c = CR_TAB_LOAD(LOG_C);
+    R.c = CR_TAB_LOAD(LOG_C_HI);
     R.l = CR_TAB_LOAD(LOG_L_HI);
   }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x);
-    double y = add_(1.0, xd);
+    uint32_t xb = f2u(x);
+    double y = add_(1.0, f2d(x));
     RedLog q = red_log(y);
-    double c = f2d(CR_TAB(R.c, LOG_C, q.i));
+    double c = hilo2d(CR_TAB(R.c, LOG_C_HI, q.i), 0u);
     double L = CR_TAB(R.l, LOG_L_HI, q.i);
     double r = fma_(q.m, c, -1.0);
     double p = fma_(mul_(r, r), logq(r), r);
-    double a = add_(fma_(i2d(q.e), LN2_D, L), p);
-    bool skip = false;
-    if (dabs(xd) <= 0x1p-26) { a = fma_(-dabs(xd), 0x1p-36, xd); skip = true; }
-    if (xd == 0.0) { a = xd; skip = true; }
-    if (xd == -1.0) { a = -INFINITY; skip = true; }
-    if (xd < -1.0) { a = NAN; skip = true; }
-    if (xd == INFINITY) { a = INFINITY; skip = true; }
-    return {a, skip};
+    // main: 2^-26 < |x| < inf and x > -1
+    return Fast{add_(fma_(i2d(q.e), LN2_D, L), p),
+                in_range(xb << 1, 0x65000002u, 0xFF000000u) && xb < 0xBF800000u};
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0) return xb;
+    if (xb == 0xBF800000u) return 0xFF800000u;  // log1p(-1) = -Inf
+    if (xb > 0xBF800000u) return 0x7FC00000u;   // x < -1
+    if (xb == 0x7F800000u) return 0x7F800000u;
+    double xd = f2d(x);
+    return f2u(cvt_f32<M>(fma_(-dabs(xd), 0x1p-36, xd)));  // x - x^2/2 just below x
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);
@@ -481,11 +516,9 @@ CR_F PH payne_hanek(uint32_t xb, const unsigned *words) {
 }
 
 CR_F double sin_r(double r, double s) {
-  return fma_(mul_(r, s), fma_(fma_(fma_(SINQ_C3, s, SINQ_C2), s, SINQ_C1), s, SINQ_C0), r);
+  return fma_(mul_(r, s), fma_(fma_(SINQ[2], s, SINQ[1]), s, SINQ[0]), r);
 }
-CR_F double cos_r(double s) {
-  return fma_(s, fma_(fma_(fma_(COSQ_C3, s, COSQ_C2), s, COSQ_C1), s, COSQ_C0), 1.0);
-}
+CR_F double cos_r(double s) { return fma_(s, fma_(fma_(COSQ[2], s, COSQ[1]), s, COSQ[0]), 1.0); }
 CR_F double sin16(double tab, int k) {
   double v = CR_TAB(tab, SIN16_HI, k & 15);
   return (k & 16) ? -v : v;
@@ -549,12 +582,11 @@ struct TrigRegs {
 };
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
-  static constexpr uint32_t E = WHICH == 2 ? 32 : 16;
+  static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
   static constexpr bool kBigArg = true;
   using Regs = TrigRegs;
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN16_HI); }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
-    double xd = f2d(x);
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
     double Sk = sin16(R.t, q.k), Ck = sin16(R.t, q.k + 8);
@@ -562,16 +594,24 @@ struct FnTrig {
     if (WHICH == 0) a = fma_(Sk, cr, mul_(Ck, sr));
     else if (WHICH == 1) a = fma_(Ck, cr, -mul_(Sk, sr));
     else a = div_fast(fma_(Sk, cr, mul_(Ck, sr)), fma_(Ck, cr, -mul_(Sk, sr)));
-    bool skip = false;
-    double ax = dabs(xd);
-    if (WHICH == 0 && ax <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
-    if (WHICH == 2 && ax <= 0x1p-13) { a = fma_(xd, 0x1p-36, xd); skip = true; }
-    if (WHICH == 1 && ax <= 0x1p-13) { a = 1.0 - 0x1p-31; skip = true; }
-    if (xd == 0.0) { a = WHICH == 1 ? 1.0 : xd; skip = true; }
-    if (ax == INFINITY) { a = NAN; skip = true; }
-    return {a, skip};
+    // main: tiny threshold < |x| < inf (sin 2^-12, cos/tan 2^-13)
+    return Fast{a, in_range(f2u(x) << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u)};
   }
-  CR_F static bool is_big(float x) { return fabs_(x) >= 0x1p17f && fabs_(x) != INFINITY; }
+  CR_F static bool is_big(float x) {
+    uint32_t az = f2u(x) << 1;
+    return az >= (0x48000000u << 1) && az < 0xFF000000u;  // 2^17 <= |x| < inf
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x), az = xb << 1;
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (az == 0xFF000000u) return 0x7FC00000u;  // sin/cos/tan(+-Inf) invalid
+    if (az == 0) return WHICH == 1 ? 0x3F800000u : xb;
+    double xd = f2d(x);
+    if (WHICH == 0) return f2u(cvt_f32<M>(fma_(-xd, 0x1p-36, xd)));  // x - x^3/6
+    if (WHICH == 2) return f2u(cvt_f32<M>(fma_(xd, 0x1p-36, xd)));   // x + x^3/3
+    return f2u(cvt_f32<M>(1.0 - 0x1p-31));                          // 1 - x^2/2
+  }
   CR_F static Fast fast(float x, const Regs &R) { return from_red(x, red_trig_small(f2d(x)), R); }
   CR_F static DD slow(float x) {
     int k;
@@ -611,8 +651,7 @@ CR_F int atan_index(double Y, double X) {
 }
 CR_F double atan_t(double t) {
   double s = mul_(t, t);
-  double q = fma_(fma_(fma_(fma_(fma_(ATANQ_C5, s, ATANQ_C4), s, ATANQ_C3), s, ATANQ_C2), s, ATANQ_C1), s,
-                  ATANQ_C0);
+  double q = fma_(fma_(fma_(ATANQ[3], s, ATANQ[2]), s, ATANQ[1]), s, ATANQ[0]);
   return fma_(mul_(t, s), q, t);
 }
 CR_F double atan2_core(double Y, double X, double tab) {
@@ -638,17 +677,21 @@ CR_F DD atan2_core_dd(DD Y, DD X) {
 }
 
 struct FnAtan {
-  static constexpr uint32_t E = 16;
+  static constexpr uint32_t E = 32;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x), ax = dabs(xd);
-    double a = atan2_core(fmin(ax, 0x1p127), 1.0, R.t);
-    a = xd < 0 ? -a : a;
-    bool skip = false;
-    if (ax <= 0x1p-12) { a = fma_(-xd, 0x1p-36, xd); skip = true; }
-    if (xd == 0.0) { a = xd; skip = true; }
-    return {a, skip};
+    uint32_t xb = f2u(x);
+    return Fast{with_sign(atan2_core(f2d(fminf(fabs_(x), 0x1p127f)), 1.0, R.t), xb),
+                in_range(xb << 1, 0x73000002u, 0xFF000002u)};  // 2^-12 < |x| <= inf
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x);
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if ((xb << 1) == 0) return xb;
+    double xd = f2d(x);
+    return f2u(cvt_f32<M>(fma_(-xd, 0x1p-36, xd)));  // x - x^3/3 just below |x|
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);
@@ -659,26 +702,32 @@ struct FnAtan {
 
 template <bool ACOS>
 struct FnAsinAcos {
-  static constexpr uint32_t E = 32;
+  static constexpr uint32_t E = 64;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    double xd = f2d(x), ax = fmin(dabs(xd), 1.0);
+    uint32_t xb = f2u(x);
+    double ax = f2d(fminf(fabs_(x), 1.0f));
     double s = sqrt_rn(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
     double a;
     if (!ACOS) {
-      a = atan2_core(ax, s, R.t);
-      a = xd < 0 ? -a : a;
+      a = with_sign(atan2_core(ax, s, R.t), xb);
     } else {
       a = atan2_core(s, ax, R.t);
-      a = xd < 0 ? add_(PI_H, -a) : a;
+      a = (int)xb < 0 ? add_(PI_H, -a) : a;
     }
-    bool skip = false;
-    if (!ACOS && dabs(xd) <= 0x1p-12) { a = fma_(xd, 0x1p-36, xd); skip = true; }
-    if (!ACOS && xd == 0.0) { a = xd; skip = true; }
-    if (ACOS && xd == 1.0) { a = 0.0; skip = true; }
-    if (dabs(xd) > 1.0) { a = NAN; skip = true; }
-    return {a, skip};
+    // asin main: 2^-12 < |x| <= 1; acos main: |x| <= 1 (acos(1) = 0 is
+    // snapped exactly by the accurate path)
+    return Fast{a, ACOS ? (xb << 1) <= 0x7F000000u : in_range(xb << 1, 0x73000002u, 0x7F000002u)};
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
+    uint32_t xb = f2u(x);
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if ((xb << 1) > 0x7F000000u) return 0x7FC00000u;  // |x| > 1
+    if ((xb << 1) == 0) return xb;                    // asin(+-0)
+    double xd = f2d(x);
+    return f2u(cvt_f32<M>(fma_(xd, 0x1p-36, xd)));   // asin: x + x^3/6 just above |x|
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x), ax = fmin(dabs(xd), 1.0);
@@ -709,15 +758,16 @@ struct FnRsqrt {
     return y;
   }
   CR_F static Fast fast(float x, const Regs &) {
-    double xd = f2d(x);
-    double a = newton(xd);
-    bool skip = false;
+    return Fast{newton(f2d(x)), f2u(x) - 1u < 0x7F7FFFFFu};  // 0 < x < inf
+  }
+  template <int M>
+  CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
-    if (xb == 0u) { a = INFINITY; skip = true; }
-    if (xb == 0x80000000u) { a = -INFINITY; skip = true; }
-    if (xb > 0x80000000u) { a = NAN; skip = true; }
-    if (xb == 0x7F800000u) { a = 0.0; skip = true; }
-    return {a, skip};
+    if (nan_bits(xb)) return quiet_bits(xb);
+    if (xb == 0u) return 0x7F800000u;
+    if (xb == 0x80000000u) return 0xFF800000u;
+    if (xb == 0x7F800000u) return 0u;
+    return 0x7FC00000u;  // x < 0
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);

@@ -55,10 +55,10 @@ __device__ __noinline__ DD slow_dd(float x) {
 // lanes, and scattered back. One pass serves up to 32 big arguments however
 // they are spread over lanes and slots.
 struct PHWarp {
-  float qx[128];
-  unsigned char qslot[128];
-  int rk[128];
-  double rr[128];
+  float qx[256];
+  unsigned short qslot[256];
+  int rk[256];
+  double rr[256];
 };
 struct PHBlock {
   unsigned words[12];
@@ -78,7 +78,7 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
     if (big[e]) {
       int pos = total + __popc(m & lt);
       w.qx[pos] = xs[e];
-      w.qslot[pos] = (unsigned char)(e * 32 + lane);
+      w.qslot[pos] = (unsigned short)(e * 32 + lane);
     }
     total += __popc(m);
   }
@@ -129,17 +129,21 @@ __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)
   Fast f[NE];
   fast_lanes<F, NE>(xs, f, R, sh);
   bool fail[NE];
-  bool any = false;
+  bool rare = false;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    ys[e] = finish<M>(f2u(xs[e]), f[e], fail[e], F::E);
-    any |= fail[e];
+    ys[e] = finish<M>(f[e], fail[e], F::E);
+    rare |= fail[e] | !f[e].main;
   }
-  if (__any_sync(kFull, any)) {
+  // Rare, warp-uniform branch: specials / tiny / saturated lanes and lanes the
+  // rounding test could not decide (accurate path, ~2^-24 of random inputs).
+  if (__any_sync(kFull, rare)) {
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      if (fail[e]) {
+      if (!f[e].main) {
+        ys[e] = F::template special<M>(xs[e]);
+      } else if (fail[e]) {
         ys[e] = slow_round<F, M>(xs[e]);
         ++cnt;
       }
@@ -148,7 +152,7 @@ __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)
   }
 }
 
-// Shared staging exists only in the trig kernels (17 KB per block).
+// Shared staging exists only in the trig kernels (34 KB per block).
 template <class F>
 __device__ __forceinline__ PHBlock *ph_storage() {
   if constexpr (IsTrig<F>::value) {
@@ -173,14 +177,25 @@ __global__ void __launch_bounds__(kThreads) k_map_vec(const float4 *x, float4 *y
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  for (uint64_t base = warp * 32; base < n4; base += nwarps * 32) {
-    uint64_t i = base + lane;
-    bool valid = i < n4;
-    float4 v = valid ? ld_stream(x + i) : make_float4(1.f, 1.f, 1.f, 1.f);
-    float xs[4] = {v.x, v.y, v.z, v.w};
-    uint32_t ys[4];
-    eval_lanes<F, M, 4>(xs, ys, R, sh, counters);
-    if (valid) st_stream(y + i, make_float4(u2f(ys[0]), u2f(ys[1]), u2f(ys[2]), u2f(ys[3])));
+  // Each warp handles 2 x 32 float4 per iteration (8 elements per lane) and
+  // requests the next iteration's two float4 before computing this one
+  // (register double buffer): four 16-byte loads in flight per lane.
+  const uint64_t stride = nwarps * 64;
+  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
+  uint64_t base = warp * 64;
+  float4 v0 = base + lane < n4 ? ld_stream(x + base + lane) : ones;
+  float4 v1 = base + 32 + lane < n4 ? ld_stream(x + base + 32 + lane) : ones;
+  for (; base < n4; base += stride) {
+    uint64_t i0 = base + lane, i1 = i0 + 32;
+    float4 n0 = i0 + stride < n4 ? ld_stream(x + i0 + stride) : ones;
+    float4 n1 = i1 + stride < n4 ? ld_stream(x + i1 + stride) : ones;
+    float xs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t ys[8];
+    eval_lanes<F, M, 8>(xs, ys, R, sh, counters);
+    if (i0 < n4) st_stream(y + i0, make_float4(u2f(ys[0]), u2f(ys[1]), u2f(ys[2]), u2f(ys[3])));
+    if (i1 < n4) st_stream(y + i1, make_float4(u2f(ys[4]), u2f(ys[5]), u2f(ys[6]), u2f(ys[7])));
+    v0 = n0;
+    v1 = n1;
   }
 }
 
@@ -220,21 +235,24 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
   }
   if (__any_sync(kFull, anyb)) coop_payne_hanek<NE>(xs, big, q, *sh);
   bool fs[NE], fc[NE];
-  bool any = false;
+  Fast a[NE], b[NE];
+  bool rare = false;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    Fast a = FnSin::from_red(xs[e], q[e], R);
-    Fast b = FnCos::from_red(xs[e], q[e], R);
-    s[e] = finish<M>(f2u(xs[e]), a, fs[e], FnSin::E);
-    c[e] = finish<M>(f2u(xs[e]), b, fc[e], FnCos::E);
-    any |= fs[e] | fc[e];
+    a[e] = FnSin::from_red(xs[e], q[e], R);
+    b[e] = FnCos::from_red(xs[e], q[e], R);
+    s[e] = finish<M>(a[e], fs[e], FnSin::E);
+    c[e] = finish<M>(b[e], fc[e], FnCos::E);
+    rare |= fs[e] | fc[e] | !a[e].main | !b[e].main;
   }
-  if (__any_sync(kFull, any)) {
+  if (__any_sync(kFull, rare)) {
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      if (fs[e]) { s[e] = slow_round<FnSin, M>(xs[e]); ++cnt; }
-      if (fc[e]) { c[e] = slow_round<FnCos, M>(xs[e]); ++cnt; }
+      if (!a[e].main) s[e] = FnSin::special<M>(xs[e]);
+      else if (fs[e]) { s[e] = slow_round<FnSin, M>(xs[e]); ++cnt; }
+      if (!b[e].main) c[e] = FnCos::special<M>(xs[e]);
+      else if (fc[e]) { c[e] = slow_round<FnCos, M>(xs[e]); ++cnt; }
     }
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);
   }
@@ -249,11 +267,16 @@ __global__ void __launch_bounds__(kThreads) k_sincos_vec(const float4 *x, float4
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  for (uint64_t base = warp * 32; base < n4; base += nwarps * 32) {
+  const uint64_t stride = nwarps * 32;
+  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
+  uint64_t base = warp * 32;
+  float4 v = base + lane < n4 ? ld_stream(x + base + lane) : ones;
+  for (; base < n4; base += stride) {
     uint64_t i = base + lane;
     bool valid = i < n4;
-    float4 v = valid ? ld_stream(x + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+    float4 vn = i + stride < n4 ? ld_stream(x + i + stride) : ones;
     float xs[4] = {v.x, v.y, v.z, v.w};
+    v = vn;
     uint32_t s[4], c[4];
     sincos_lanes<M, 4>(xs, s, c, R, sh, counters);
     if (valid) {
@@ -296,12 +319,20 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 template <class F>
-__device__ __forceinline__ void finish4(uint32_t xb, Fast f, uint32_t (&y)[4], bool &fail) {
-  y[0] = finish<RNE>(xb, f, fail, F::E);
-  bool d;
-  y[1] = finish<RZ>(xb, f, d, F::E);
-  y[2] = finish<RU>(xb, f, d, F::E);
-  y[3] = finish<RD>(xb, f, d, F::E);
+__device__ __forceinline__ void finish4(float x, Fast f, uint32_t (&y)[4], bool &fail) {
+  if (f.main) {
+    y[0] = finish<RNE>(f, fail, F::E);
+    bool d;
+    y[1] = finish<RZ>(f, d, F::E);
+    y[2] = finish<RU>(f, d, F::E);
+    y[3] = finish<RD>(f, d, F::E);
+  } else {
+    fail = false;
+    y[0] = F::template special<RNE>(x);
+    y[1] = F::template special<RZ>(x);
+    y[2] = F::template special<RU>(x);
+    y[3] = F::template special<RD>(x);
+  }
 }
 __device__ __forceinline__ void round4(DD v, uint32_t (&y)[4]) {
   y[0] = round_dd<RNE>(v.hi, v.lo);
@@ -358,9 +389,8 @@ __global__ void __launch_bounds__(kThreads) k_sweep(uint32_t chunk_lo, uint64_t 
       uint32_t y[4];
       bool fail;
       uint32_t xb = pb + e;
-      finish4<F>(xb, f[e], y, fail);
-      bool xnan = (xb & 0x7FFFFFFFu) > 0x7F800000u;
-      if (fail || (FORCE && !f[e].skip && !xnan)) {
+      finish4<F>(xs[e], f[e], y, fail);
+      if (fail || (FORCE && f[e].main)) {
         round4(slow_dd<F>(xs[e]), y);
         ++nslow;
       }
@@ -401,15 +431,14 @@ __global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, ui
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t xb = pb + e;
-      bool xnan = (xb & 0x7FFFFFFFu) > 0x7F800000u;
       Fast a = FnSin::from_red(xs[e], q[e], R);
       Fast b = FnCos::from_red(xs[e], q[e], R);
       uint32_t ys[4], yc[4];
       bool fs, fc;
-      finish4<FnSin>(xb, a, ys, fs);
-      finish4<FnCos>(xb, b, yc, fc);
-      if (fs || (FORCE && !a.skip && !xnan)) { round4(slow_dd<FnSin>(xs[e]), ys); ++nslow; }
-      if (fc || (FORCE && !b.skip && !xnan)) { round4(slow_dd<FnCos>(xs[e]), yc); ++nslow; }
+      finish4<FnSin>(xs[e], a, ys, fs);
+      finish4<FnCos>(xs[e], b, yc, fc);
+      if (fs || (FORCE && a.main)) { round4(slow_dd<FnSin>(xs[e]), ys); ++nslow; }
+      if (fc || (FORCE && b.main)) { round4(slow_dd<FnCos>(xs[e]), yc); ++nslow; }
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         acc[m] += mix64(((uint64_t)ys[m] << 32) | xb);
@@ -444,7 +473,7 @@ inline int max_blocks(K kernel) {
 inline unsigned grid_for(uint64_t work_warps32, int maxb) {
   // work_warps32 = number of 32-lane slots; one warp per slot per pass
   uint64_t blocks = (work_warps32 + kWarps - 1) / kWarps;
-  if (blocks > (uint64_t)maxb) blocks = maxb;
+  if (blocks > 4ull * (uint64_t)maxb) blocks = 4ull * (uint64_t)maxb;  // 4 waves: better tail balance
   return (unsigned)(blocks ? blocks : 1);
 }
 
@@ -456,7 +485,7 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
   bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
   uint64_t n4 = aligned ? n / 4 : 0;
   if (n4) {
-    k_map_vec<F, M><<<grid_for((n4 + 31) / 32, mb_vec), kThreads, 0, s>>>(
+    k_map_vec<F, M><<<grid_for((n4 + 63) / 64, mb_vec), kThreads, 0, s>>>(
         (const float4 *)x, (float4 *)y, n4, ctr);
   }
   uint64_t rem = n - 4 * n4;

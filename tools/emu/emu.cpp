@@ -23,10 +23,10 @@ static uint32_t eval1(float x, int force, uint64_t *slow) {
   } else {
     f = F::fast(x, R);
   }
+  if (!f.main) return F::template special<M>(x);
   bool fail;
-  uint32_t y = finish<M>(f2u(x), f, fail, F::E);
-  bool xnan = (f2u(x) & 0x7FFFFFFFu) > 0x7F800000u;
-  if (fail || (force && !f.skip && !xnan)) {
+  uint32_t y = finish<M>(f, fail, F::E);
+  if (fail || force) {
     ++*slow;
     DD v = F::slow(x);
     y = round_dd<M>(v.hi, v.lo);

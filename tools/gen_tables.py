@@ -102,12 +102,12 @@ def arr(name, vals, ctype="double"):
 
 
 def scalar(name, v):
-    emit(f"#define {name} {hx(v)}")
+    # constant-bank scalar: FP64 instructions read it as a c[] operand
+    emit(f"static CR_CONST double {name} = {hx(v)};")
 
 
 def poly_block(name, cs):
-    for i, c in enumerate(cs):
-        scalar(f"{name}_C{i}", d(c))
+    arr(name, [d(c) for c in cs])
 
 
 # ------------------------------------------------------------------ exp ----
@@ -122,13 +122,12 @@ def gen_exp():
     arr("EXP2J_LO", [dd(t)[1] for t in T])
     # e^r - 1 = r + r^2 * Q(r), Q degree 4 (fast path)
     g = lambda r: (mp.expm1(r) - r) / r ** 2 if r != 0 else mp.mpf(1) / 2
-    for deg in (3, 4):
+    for deg, name in ((3, "EXPQ3"), (4, "EXPQ")):
         cs, _ = chebfit(g, -R_EXP, R_EXP, deg)
         csd = [mp.mpf(d(c)) for c in cs]
         err = rel_err_of(lambda r: r + r * r * horner(csd, r), mp.expm1, -R_EXP, R_EXP)
         report.append(f"expm1 poly r+r^2*Q deg(Q)={deg}: max rel err 2^{float(mp.log(err, 2)):.1f}")
-        if deg == 4:
-            poly_block("EXPQ", csd)
+        poly_block(name, csd)
     h, m, l = split3(LN2 / 16, 40, 40)
     scalar("LN2_16_H", h); scalar("LN2_16_M", m); scalar("LN2_16_L", l)
     scalar("INV_LN2_16", d(16 / LN2))
@@ -189,19 +188,22 @@ def gen_log():
         L2.append(-mp.log(c, 2))
         L10.append(-mp.log(c, 10))
     arr("LOG_C", cs_)
+    assert all((int.from_bytes(__import__("struct").pack("<d", c), "little") & 0xFFFFFFFF) == 0 for c in cs_)
+    emit("static CR_CONST int LOG_C_HI[16] = {")
+    emit("    " + ", ".join(str(int.from_bytes(__import__("struct").pack("<d", c), "little") >> 32) for c in cs_) + ",")
+    emit("};")
     arr("LOG_L_HI", [dd(v)[0] for v in L]); arr("LOG_L_LO", [dd(v)[1] for v in L])
     arr("LOG2_L_HI", [dd(v)[0] for v in L2]); arr("LOG2_L_LO", [dd(v)[1] for v in L2])
     arr("LOG10_L_HI", [dd(v)[0] for v in L10]); arr("LOG10_L_LO", [dd(v)[1] for v in L10])
     report.append(f"log r range [{float(rmin):.5f}, {float(rmax):.5f}]")
     a, b = rmin * mp.mpf("1.001"), rmax * mp.mpf("1.001")
     g = lambda r: (mp.log1p(r) - r) / r ** 2 if r != 0 else -mp.mpf(1) / 2
-    for deg in (6, 7):
+    for deg in (6,):
         cs, _ = chebfit(g, a, b, deg)
         csd = [mp.mpf(d(c)) for c in cs]
         err = rel_err_of(lambda r: r + r * r * horner(csd, r), mp.log1p, a, b)
         report.append(f"log1p poly r+r^2*Q deg(Q)={deg}: max rel err 2^{float(mp.log(err, 2)):.1f}")
-        if deg == 7:
-            poly_block("LOGQ", csd)
+        poly_block("LOGQ", csd)
     h, m, l = split3(LN2, 40, 40)
     scalar("LN2_H", h); scalar("LN2_M", m); scalar("LN2_L", l)
     scalar("INV_LN2", d(1 / LN2)); scalar("INV_LN2_L", d(1 / LN2 - d(1 / LN2)))
@@ -220,16 +222,16 @@ def gen_trig():
     arr("SIN16_HI", [dd(v)[0] for v in S]); arr("SIN16_LO", [dd(v)[1] for v in S])
     R = PI / 32 * mp.mpf("1.0005")
     gs = lambda s: (mp.sin(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 6
-    cs, _ = chebfit(gs, mp.mpf(0), R ** 2, 3)
+    cs, _ = chebfit(gs, mp.mpf(0), R ** 2, 2)
     csd = [mp.mpf(d(c)) for c in cs]
     err = rel_err_of(lambda r: r + r ** 3 * horner(csd, r * r), mp.sin, -R, R)
-    report.append(f"sin poly deg 3 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    report.append(f"sin poly deg 2 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
     poly_block("SINQ", csd)
     gc = lambda s: (mp.cos(mp.sqrt(s)) - 1) / s if s > 0 else -mp.mpf(1) / 2
-    cs, _ = chebfit(gc, mp.mpf(0), R ** 2, 3)
+    cs, _ = chebfit(gc, mp.mpf(0), R ** 2, 2)
     csd = [mp.mpf(d(c)) for c in cs]
     err = rel_err_of(lambda r: 1 + r * r * horner(csd, r * r), mp.cos, -R, R)
-    report.append(f"cos poly deg 3 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    report.append(f"cos poly deg 2 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
     poly_block("COSQ", csd)
     scalar("INV_PI_16", d(16 / PI))
     h, m, l = split3(PI / 16, 33, 33)
@@ -269,13 +271,12 @@ def gen_atrig():
     T = mp.tan(PI / 60 + mp.mpf("0.0065"))
     report.append(f"atan t bound {float(T):.5f}")
     g = lambda s: (mp.atan(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 3
-    for deg in (4, 5):
+    for deg in (3,):
         cs, _ = chebfit(g, mp.mpf(0), T ** 2, deg)
         csd = [mp.mpf(d(c)) for c in cs]
         err = rel_err_of(lambda t: t + t ** 3 * horner(csd, t * t), mp.atan, -T, T)
         report.append(f"atan poly deg {deg} in t^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
-        if deg == 5:
-            poly_block("ATANQ", csd)
+        poly_block("ATANQ", csd)
     h, l = dd(PI / 30)
     scalar("PI_30_H", h); scalar("PI_30_L", l)
     h, l = dd(PI)
