@@ -56,15 +56,32 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region (NVML every
+    5 ms; falls back to nvidia-smi polling when NVML is unavailable)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
 
     def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, rs))
+                self._stop.wait(0.005)
+            return
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -73,8 +90,9 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"],
                                      capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                v = [t.strip() for t in out.split(",")]
+                bits = sum(b for b, on in zip((0x8, 0x40, 0x20, 0x4), v[2:6]) if on.lower() == "active")
+                self.samples.append((float(v[0]), float(v[1]), bits))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -90,15 +108,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for bit, name in self.REASONS.items() if s[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(s[1] for s in self.samples)),
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml 5 ms"}
 
 
 def dist_init():
@@ -175,48 +189,25 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------------ sweep ----
 def run_sweep(rank, world, fns):
-    """Exhaustive 2^32 sweep of `fns`, chunks sharded across ranks, one
-    all_reduce of the per-chunk hashes (NCCL); returns (seconds, mismatches)."""
+    """Exhaustive 2^32 x 4-mode sweep of `fns`: chunk ranges sharded across
+    ranks (paper_2605_15547_b200/sweep.py), one all_reduce (NCCL) of the
+    per-chunk hash table; seconds = max over ranks of the device time."""
     import torch
     import paper_2605_15547_b200 as crvec
-    per = 4096 // world
-    lo, hi = rank * per, (rank + 1) * per
-    names = list(fns)
-    hashes = torch.zeros((len(names) + 1, 4096, 4), dtype=torch.int64, device="cuda")
-    ctr = torch.zeros(4, dtype=torch.int64, device="cuda")
-    L = crvec.lib()
-    stream = torch.cuda.current_stream()
+    from paper_2605_15547_b200 import sweep
     barrier(world)
     torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for i, name in enumerate(names):
-        h = hashes[i, lo:hi]
-        h2 = hashes[len(names), lo:hi] if name == "sincosf" else None
-        rc = L.crvec_sweep_f32(crvec.FN_IDS[name], lo, hi, h.data_ptr(),
-                               h2.data_ptr() if h2 is not None else None, ctr.data_ptr(), 0,
-                               __import__("ctypes").c_void_p(stream.cuda_stream))
-        assert rc == 0, rc
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(hashes)
-    ev1.record(stream)
+    ev0.record(s)
+    rows, table, _ = sweep.run(fns, sweep.gpu_evaluator(), rank, world, device="cuda")
+    ev1.record(s)
     torch.cuda.synchronize()
     secs = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
-    mism = 0
-    checked = 0
-    hh = hashes.cpu().numpy().view(np.uint64)
-    for i, name in enumerate(names):
-        if name == "sincosf":
-            pairs = [("sin", hh[i]), ("cos", hh[len(names)])]
-        else:
-            pairs = [(crvec.ORACLE_NAME[name], hh[i])]
-        for g, arr in pairs:
-            p = os.path.join(ROOT, "tests", "golden", "sweep", g + ".npy")
-            if os.path.exists(p):
-                mism += int((np.load(p) != arr).any(1).sum())
-                checked += 1
-    return secs, mism, checked, int(ctr[0].item())
+    res = sweep.compare(rows, table, ROOT, crvec.ORACLE_NAME)
+    mism = sum(len(v) for v in res.values() if v is not None)
+    checked = sum(1 for v in res.values() if v is not None)
+    return secs, mism, checked
 
 
 # --------------------------------------------------------------- our arm -----
@@ -296,10 +287,9 @@ def run_crvec(args, rank, world, local):
     # ---- exhaustive sweep (sharded across ranks)
     sweep = None
     if not args.no_sweep:
-        secs_sw, mism, checked, nacc = run_sweep(rank, world, crvec.F32_FUNCS + ["sincosf"])
+        secs_sw, mism, checked = run_sweep(rank, world, crvec.F32_FUNCS + ["sincosf"])
         sweep = {"seconds": secs_sw, "functions": 19, "modes": 4, "patterns": 2 ** 32,
-                 "mismatching_chunks": mism, "golden_sets_checked": checked,
-                 "accurate_path_lanes": nacc, "ranks": world,
+                 "mismatching_chunks": mism, "golden_sets_checked": checked, "ranks": world,
                  "collective": "one NCCL all_reduce of 20x4096x4 u64 chunk hashes" if world > 1 else None}
 
     cpu = None
@@ -335,7 +325,7 @@ def run_crvec(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="crvec", choices=["crvec", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)

@@ -128,6 +128,10 @@ int crvec_exp2(const double *x, double *y, size_t n, crvec_mode_t mode, crvec_st
 int crvec_log(const double *x, double *y, size_t n, crvec_mode_t mode, crvec_stats_t *stats);
 int crvec_exp2_dev(const double *x, double *y, size_t n, crvec_mode_t mode, void *stream);
 int crvec_log_dev(const double *x, double *y, size_t n, crvec_mode_t mode, void *stream);
+/* Verification entry point: every non-special lane through the binary64
+ * accurate path (fn 0 = exp2, 1 = log); device pointers. */
+int crvec_f64_accurate_dev(int fn, const double *x, double *y, size_t n, crvec_mode_t mode,
+                           void *stream);
 
 /* ---- exhaustive binary32 sweep (verify) ----
  * For chunks [chunk_lo, chunk_hi) of 2^20 bit patterns (chunk c = patterns

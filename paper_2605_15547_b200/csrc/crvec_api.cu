@@ -20,6 +20,8 @@ void register_trig(FnEntry *t);
 void register_atrig(FnEntry *t);
 int f64_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
                  unsigned long long *ctr);
+int f64_accurate_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
+                          unsigned long long *ctr);
 }  // namespace crvec
 
 using namespace crvec;
@@ -258,6 +260,15 @@ int crvec_exp2_dev(const double *x, double *y, size_t n, crvec_mode_t m, void *s
 }
 int crvec_log_dev(const double *x, double *y, size_t n, crvec_mode_t m, void *s) {
   return eval_f64_dev(1, x, y, n, m, s);
+}
+int crvec_f64_accurate_dev(int fn, const double *x, double *y, size_t n, crvec_mode_t m,
+                           void *stream) {
+  if (fn < 0 || fn > 1 || m < 0 || m > 3 || (n && (!x || !y))) return CRVEC_EINVAL;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  return f64_accurate_dispatch(fn, x, y, n, m, (cudaStream_t)stream, D->counters + 1) ? CRVEC_ECUDA
+                                                                                       : CRVEC_OK;
 }
 
 #endif

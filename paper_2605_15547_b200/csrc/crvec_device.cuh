@@ -238,6 +238,16 @@ CR_F bool nan_bits(uint32_t xb) { return (xb << 1) > 0xFF000000u; }
 // quiet(x): payload and sign kept (ref: proj/include/crvec/fpbits.hpp:101-102).
 CR_F uint32_t quiet_bits(uint32_t xb) { return xb | 0x00400000u; }
 
+// sqrt(a) for a in [0, 1] to ~2^-52 relative: MUFU seed, one rsqrt Newton
+// step, one Karp-Markstein correction (7 FP64 ops; a = 0 -> 0).
+CR_F double sqrt_fast(double a) {
+  double y = rsqrt_approx(a);
+  y = fma_(mul_(y, 0.5), fma_(-mul_(a, y), y, 1.0), y);
+  double s = mul_(a, y);
+  s = fma_(fma_(-s, s, a), mul_(y, 0.5), s);
+  return a > 0.0 ? s : 0.0;
+}
+
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);
 // valid while the result stays normal.
 CR_F double scale2(double a, int e) { return hilo2d(d2hi(a) + (e << 20), d2lo(a)); }

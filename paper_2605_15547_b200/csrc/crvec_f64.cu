@@ -126,6 +126,42 @@ cudaError_t launch64(const double *x, double *y, uint64_t n, cudaStream_t s,
   return cudaGetLastError();
 }
 
+// Verification: every lane through the accurate path (one lane per thread).
+template <int FN, int M>
+__global__ void __launch_bounds__(kT64) k_f64_accurate(const double *x, double *y, uint64_t n,
+                                                       unsigned long long *ctr) {
+  uint64_t i = (uint64_t)blockIdx.x * kT64 + threadIdx.x;
+  int und = 0;
+  if (i < n) {
+    double xv = x[i];
+    F64Tab *T = nullptr;
+    (void)T;
+    bool special;
+    if (FN == 0) special = xv != xv || xv >= 1024.0 || xv <= -1075.0 || xv == floor(xv) || dabs(xv) <= 0x1p-55;
+    else special = xv != xv || xv <= 0.0 || xv == INFINITY || xv == 1.0;
+    if (special) {
+      // specials / exact / rule lanes have no accurate-path form: fast path
+      __shared__ F64Tab Ts;  // unused by the special branches
+      y[i] = FN == 0 ? exp2d_fast<M>(xv, Ts).y : logd_fast<M>(xv, Ts).y;
+    } else {
+      y[i] = accurate<FN, M>(xv, &und);
+    }
+  }
+  if (und) atomicAdd(ctr + 1, 1ull);
+}
+
+int f64_accurate_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
+                          unsigned long long *ctr) {
+  using K = void (*)(const double *, double *, uint64_t, unsigned long long *);
+  static const K tab[2][4] = {
+      {k_f64_accurate<0, RNE>, k_f64_accurate<0, RZ>, k_f64_accurate<0, RU>, k_f64_accurate<0, RD>},
+      {k_f64_accurate<1, RNE>, k_f64_accurate<1, RZ>, k_f64_accurate<1, RU>, k_f64_accurate<1, RD>}};
+  if (fn < 0 || fn > 1 || mode < 0 || mode > 3) return -1;
+  if (!n) return 0;
+  tab[fn][mode]<<<(unsigned)((n + kT64 - 1) / kT64), kT64, 0, s>>>(x, y, n, ctr);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 // ctr: [1] fast_undecided, [2] accurate_undecided (device counters of the API)
 int f64_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
                  unsigned long long *ctr) {

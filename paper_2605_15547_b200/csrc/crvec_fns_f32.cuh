@@ -221,16 +221,17 @@ struct FnExpm1 {
 struct HypParts {
   double Sa, Ca, sr, cr;
 };
-CR_F HypParts hyp_parts(double ax, double tab, double tabl) {
+// Fast path uses the rounded table (2^-54 relative per entry): for k = +-1 the
+// difference E+ - E- loses ~5 bits, which the sinh/tanh tolerances cover.
+CR_F HypParts hyp_parts(double ax, double tab) {
   RedExp q = red_exp(ax);
   int kp = q.k, km = -q.k;
-  double s1 = scale2(1.0, kp >> 4), s2 = scale2(1.0, km >> 4);
-  double Ep = CR_TAB(tab, EXP2J_HI, kp & 15) * s1, Elp = CR_TAB(tabl, EXP2J_LO, kp & 15) * s1;
-  double Em = CR_TAB(tab, EXP2J_HI, km & 15) * s2, Elm = CR_TAB(tabl, EXP2J_LO, km & 15) * s2;
+  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp & 15), kp >> 4);
+  double Em = scale2(CR_TAB(tab, EXP2J_HI, km & 15), km >> 4);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ[2], s, SINHQ[1]), s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(fma_(COSHQ[2], s, COSHQ[1]), s, COSHQ[0]), 1.0);
-  double Sa = mul_(add_(sub_(Ep, Em), sub_(Elp, Elm)), 0.5);
+  double Sa = mul_(sub_(Ep, Em), 0.5);
   double Ca = mul_(add_(Ep, Em), 0.5);
   return {Sa, Ca, sr, cr};
 }
@@ -259,15 +260,12 @@ CR_F HypDD hyp_parts_dd(double ax) {
 }
 
 struct FnSinh {
-  static constexpr uint32_t E = 16;
-  struct Regs { double t, tl; };
-  CR_F static void load(Regs &R) {
-    R.t = CR_TAB_LOAD(EXP2J_HI);
-    R.tl = CR_TAB_LOAD(EXP2J_LO);
-  }
+  static constexpr uint32_t E = 128;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t, R.tl);
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
     return Fast{with_sign(fma_(h.Sa, h.cr, mul_(h.Ca, h.sr)), xb),
                 in_range(xb << 1, 0x73000002u, 0xFF000000u)};  // 2^-12 < |x| < inf
   }
@@ -288,14 +286,11 @@ struct FnSinh {
 };
 
 struct FnCosh {
-  static constexpr uint32_t E = 8;
-  struct Regs { double t, tl; };
-  CR_F static void load(Regs &R) {
-    R.t = CR_TAB_LOAD(EXP2J_HI);
-    R.tl = CR_TAB_LOAD(EXP2J_LO);
-  }
+  static constexpr uint32_t E = 16;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
-    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t, R.tl);
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
     return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)),
                 in_range(f2u(x) << 1, 0x72000002u, 0xFF000000u)};  // 2^-13 < |x| < inf
   }
@@ -314,15 +309,12 @@ struct FnCosh {
 };
 
 struct FnTanh {
-  static constexpr uint32_t E = 32;
-  struct Regs { double t, tl; };
-  CR_F static void load(Regs &R) {
-    R.t = CR_TAB_LOAD(EXP2J_HI);
-    R.tl = CR_TAB_LOAD(EXP2J_LO);
-  }
+  static constexpr uint32_t E = 256;
+  struct Regs { double t; };
+  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 10.0f)), R.t, R.tl);
+    HypParts h = hyp_parts(f2d(fminf(fabs_(x), 10.0f)), R.t);
     double sh = fma_(h.Sa, h.cr, mul_(h.Ca, h.sr));
     double ch = fma_(h.Ca, h.cr, mul_(h.Sa, h.sr));
     return Fast{with_sign(div_fast(sh, ch), xb),
@@ -431,9 +423,13 @@ struct FnLog1p {
     double L = CR_TAB(R.l, LOG_L_HI, q.i);
     double r = fma_(q.m, c, -1.0);
     double p = fma_(mul_(r, r), logq(r), r);
-    // main: 2^-26 < |x| < inf and x > -1
-    return Fast{add_(fma_(i2d(q.e), LN2_D, L), p),
-                in_range(xb << 1, 0x65000002u, 0xFF000000u) && xb < 0xBF800000u};
+    double a = add_(fma_(i2d(q.e), LN2_D, L), p);
+    // |x| <= 2^-26 is ~40% of all bit patterns: keep its rule on the main
+    // path (x - x^2/2 lies just below x; the value is far from boundaries).
+    double xd = f2d(x);
+    if ((xb << 1) <= 0x65000000u) a = fma_(-dabs(xd), 0x1p-36, xd);
+    // main: 0 < |x| < inf and x > -1
+    return Fast{a, in_range(xb << 1, 2u, 0xFF000000u) && xb < 0xBF800000u};
   }
   template <int M>
   CR_F static uint32_t special(float x) {
@@ -448,12 +444,19 @@ struct FnLog1p {
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);
+    // tiny |x|: the main path's rule (x - x^2/2 strictly inside the gap below
+    // x) — a plain DD here would be snapped to x by round_dd.
+    if ((f2u(x) << 1) <= 0x65000000u) return DD{xd, -dabs(xd) * 0x1p-36};
     DD y = two_sum(1.0, xd);  // 1 + x = y.hi + y.lo exactly
     RedLog q = red_log(y.hi);
     DD pm = two_prod(q.m, (double)LOG_C[q.i]);
     DD r = fast_two_sum(sub_(pm.hi, 1.0), pm.lo);
     DD v = FnLogB<0>::log_dd_core(q.e, q.i, r);
-    return dd_add_d(v, y.lo / y.hi);
+    // log(1 + x) = log(y.hi) + log1p(u), u = y.lo / y.hi (|u| <= 2^-53, or
+    // u = x itself when x is tiny and y.hi == 1): u - u^2/2 + u^3/3 - u^4/4.
+    double u = y.lo / y.hi;
+    double tail = mul_(u, fma_(u, fma_(u, fma_(u, -0.25, 1.0 / 3.0), -0.5), 0.0));
+    return dd_add(v, fast_two_sum(u, tail));
   }
 };
 
@@ -708,7 +711,7 @@ struct FnAsinAcos {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     double ax = f2d(fminf(fabs_(x), 1.0f));
-    double s = sqrt_rn(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
+    double s = sqrt_fast(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
     double a;
     if (!ACOS) {
       a = with_sign(atan2_core(ax, s, R.t), xb);

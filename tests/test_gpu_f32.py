@@ -138,7 +138,9 @@ def test_accurate_path_self_check(cuda, name):
     """Route EVERY non-special lane through the double-double accurate path
     (the rarely-taken fallback) over 64 spread chunks: must still match."""
     g = _golden(crvec.ORACLE_NAME[name])
-    for lo in range(0, 4096, 512):
+    total = 0
+    for lo in list(range(0, 4096, 512)) + [1008, 1016, 3056]:
         h, _, n_acc = crvec.sweep_f32(name, lo, lo + 8, force_accurate=True)
-        assert n_acc > 0
+        total += n_acc
         assert (h == g[lo:lo + 8]).all(), f"{name}: forced-accurate chunk mismatch at {lo}"
+    assert total > 1 << 20, total  # millions of lanes really went through the accurate path

@@ -1,0 +1,121 @@
+"""GPU parity tests for the binary64 CR exp2 / log (config C5).
+
+Bit-exact against the oracle's ziv_correctly_round_f64 (the reference's own
+algorithm, ref: proj/src/oracle.cpp:326-345, pinned in tests/test_oracle.py)
+in all four modes: the paper's ranges, wide ranges, specials and exact cases,
+a seeded hard-to-round set, and the accurate path on its own.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2605_15547_b200 as crvec
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(oracle, name, x, got_fn):
+    xb = np.ascontiguousarray(x, dtype=np.float64).view(np.uint64)
+    want = oracle.f64(name, xb, None)
+    for mode in range(4):
+        got = got_fn(x, mode).view(np.uint64)
+        bad = np.nonzero(got != want[:, mode])[0]
+        assert len(bad) == 0, (name, mode, [(float(x[i]), hex(int(got[i])), hex(int(want[i, mode])))
+                                             for i in bad[:5]])
+
+
+def _host(name):
+    return lambda x, m: crvec._f64(name, np.ascontiguousarray(x, np.float64), m, None)
+
+
+def _dev(cuda, name):
+    def f(x, m):
+        t = cuda.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+        return crvec._f64(name, t, m, None).cpu().numpy()
+    return f
+
+
+def specials_exp2():
+    ints = np.arange(-1080, 1030, dtype=np.float64)
+    return np.concatenate([ints, ints + 0.5, [0.0, -0.0, np.inf, -np.inf, np.nan, 2.0 ** -56, -2.0 ** -56,
+                                              2.0 ** -54, -2.0 ** -54, 1023.999999999, -1074.999,
+                                              -1075.0, -1075.5, -1022.5, 1e300, -1e300, 5e-324]])
+
+
+def specials_log():
+    return np.concatenate([2.0 ** np.arange(-1074, 1024, dtype=np.float64),
+                           [0.0, -0.0, np.inf, -np.inf, np.nan, -1.0, 1.0, 5e-324, 2.2250738585072014e-308,
+                            1.7976931348623157e308, 0.75, 1.5, 0.7499999999999999, 1.4999999999999998]])
+
+
+def hard_log():
+    """Algebraic families close to rounding boundaries:
+    log(1 + 2^-k), log(1 - 2^-k), log(2^j (1 + 2^-k))."""
+    k = np.arange(20, 53, dtype=np.float64)
+    base = np.concatenate([1 + 2.0 ** -k, 1 - 2.0 ** -k, 1 + 3 * 2.0 ** -k])
+    js = np.array([-1000, -100, -7, -1, 1, 5, 64, 500, 1000], dtype=np.float64)
+    return np.concatenate([base] + [base * 2.0 ** j for j in js])
+
+
+def hard_exp2():
+    k = np.arange(14, 56, dtype=np.float64)
+    return np.concatenate([2.0 ** -k, -(2.0 ** -k), 1 + 2.0 ** -k, 10 - 2.0 ** -k, -20 + 2.0 ** -k,
+                           1023 + 2.0 ** -k, -1074 + 2.0 ** -k])
+
+
+def test_exp2_paper_range_and_wide(cuda, oracle):
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-20, 20, 1 << 18), rng.uniform(-1075, 1024, 1 << 16),
+                        rng.integers(0, 2 ** 64, 1 << 14, dtype=np.uint64).view(np.float64)])
+    _check(oracle, "exp2", x, _dev(cuda, "exp2"))
+
+
+def test_log_paper_range_and_wide(cuda, oracle):
+    rng = np.random.default_rng(6)
+    x = np.concatenate([rng.uniform(0.125, 8, 1 << 18), rng.uniform(0.5, 2, 1 << 16),
+                        rng.integers(0, 2 ** 63, 1 << 14, dtype=np.uint64).view(np.float64)])
+    _check(oracle, "log", x, _dev(cuda, "log"))
+
+
+def test_specials_exact_and_hard_sets_host_path(cuda, oracle):
+    _check(oracle, "exp2", np.concatenate([specials_exp2(), hard_exp2()]), _host("exp2"))
+    _check(oracle, "log", np.concatenate([specials_log(), hard_log()]), _host("log"))
+
+
+def _accurate_only(cuda, fn):
+    L = crvec.lib()
+    L.crvec_f64_accurate_dev.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                         ctypes.c_int, ctypes.c_void_p]
+
+    def f(x, m):
+        t = cuda.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+        y = cuda.empty_like(t)
+        s = cuda.cuda.current_stream()
+        assert L.crvec_f64_accurate_dev(fn, t.data_ptr(), y.data_ptr(), t.numel(), m,
+                                        ctypes.c_void_p(s.cuda_stream)) == 0
+        s.synchronize()
+        return y.cpu().numpy()
+    return f
+
+
+def test_accurate_path_alone(cuda, oracle):
+    """The ballot-compacted 256-bit accurate path, on every lane."""
+    rng = np.random.default_rng(7)
+    xe = np.concatenate([rng.uniform(-20, 20, 4096), rng.uniform(-1075, -1022, 2048), hard_exp2(),
+                         rng.uniform(1000, 1024, 512)])
+    _check(oracle, "exp2", xe, _accurate_only(cuda, 0))
+    xl = np.concatenate([rng.uniform(0.125, 8, 4096), hard_log(),
+                         rng.integers(1, 2 ** 52, 1024, dtype=np.uint64).view(np.float64)])
+    _check(oracle, "log", xl, _accurate_only(cuda, 1))
+
+
+def test_fast_path_stats(cuda):
+    """FastPathStats: undecided rate on the paper's ranges (SPEC target < 2^-15)."""
+    rng = np.random.default_rng(8)
+    for name, x in (("exp2", rng.uniform(-20, 20, 1 << 22)), ("log", rng.uniform(0.125, 8, 1 << 22))):
+        st = crvec.FastPathStats()
+        crvec._f64(name, x, 0, st)
+        assert st.lanes == x.size
+        assert st.undecided / x.size < 2.0 ** -15, (name, st)
+        assert st.accurate_undecided == 0

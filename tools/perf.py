@@ -16,7 +16,11 @@ import paper_2605_15547_b200 as crvec  # noqa: E402
 from tests.inputs import log_family_input, mixed_f32, trig_input  # noqa: E402
 
 
-def inputs(name, n):
+def inputs(name, n, dist="config"):
+    if dist == "uniform":
+        rng = np.random.default_rng(7)
+        lo, hi = __import__("tests.inputs", fromlist=["RANGES"]).RANGES[name]
+        return rng.uniform(lo, hi, n).astype(np.float32).view(np.uint32)
     if name in ("logf", "log2f", "log10f", "log1pf"):
         return log_family_input(name, n)
     if name in ("sinf", "cosf", "tanf", "sincosf"):
@@ -32,6 +36,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--fn", nargs="*")
     ap.add_argument("--mode", type=int, default=0)
+    ap.add_argument("--dist", default="config", choices=["config", "uniform"])
+    ap.add_argument("--no-f64", action="store_true")
     a = ap.parse_args()
     n = 1 << a.n
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
@@ -40,11 +46,13 @@ def main():
     s = torch.cuda.current_stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     names = a.fn or (crvec.F32_FUNCS + ["sincosf"])
+    want64 = (not a.fn and not a.no_f64) or (a.fn and "f64" in a.fn)
+    names = [nm for nm in names if nm != "f64"]
     y = torch.empty(n, dtype=torch.float32, device="cuda")
     y2 = torch.empty(n, dtype=torch.float32, device="cuda")
     rows = []
     for name in names:
-        x = torch.from_numpy(inputs(name, n).view(np.float32)).cuda()
+        x = torch.from_numpy(inputs(name, n, a.dist).view(np.float32)).cuda()
         fid = crvec.FN_IDS[name]
         for _ in range(3):
             L.crvec_eval_f32_dev(fid, x.data_ptr(), y.data_ptr(), y2.data_ptr(), n, a.mode, sp)
@@ -65,7 +73,7 @@ def main():
         print(json.dumps(r), flush=True)
         del x
     # binary64
-    if hasattr(L, "crvec_exp2_dev") and not a.fn:
+    if hasattr(L, "crvec_exp2_dev") and want64:
         rng = np.random.default_rng(5)
         n64 = 1 << 26
         for name, xs in (("exp2", rng.uniform(-20, 20, n64)), ("log", rng.uniform(0.125, 8, n64))):
