@@ -145,6 +145,17 @@ int crvec_f64_accurate_dev(int fn, const double *x, double *y, size_t n, crvec_m
 int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *hashes,
                     uint64_t *hashes2, uint64_t *counters, int force_accurate, void *stream);
 
+/* ---- hard-case screen (GPU worst-case finder) ----
+ * Evaluates every pattern of chunks [chunk_lo, chunk_hi) on the double-double
+ * path and appends inputs whose value lies within rel_threshold (relative) of a
+ * binary32 rounding boundary: out_bits / out_dist (device, capacity entries),
+ * *count (device, caller-zeroed) = total candidates found. The GPU analogue of
+ * the reference's hardest_case_search (ref: proj/src/oracle.cpp:565-580); the
+ * exact ranking is then confirmed by the oracle's boundary distance. */
+int crvec_hardcase_scan_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, double rel_threshold,
+                            uint32_t *out_bits, double *out_dist, uint64_t capacity,
+                            uint64_t *count, void *stream);
+
 /* ---- accounting / errors ---- */
 int crvec_stats_get(crvec_stats_t *out);   /* cumulative since load / last reset */
 int crvec_stats_reset(void);

@@ -432,7 +432,7 @@ static const int ziv_ladder[] = {96, 160, 256, 512, 1024, 2048, 4096};
 
 /* Per-thread MPFR scratch (ref: proj/src/oracle.cpp:93-124). */
 typedef struct {
-  mpfr_t x, v, err, lo, hi;
+  mpfr_t x, v, err, lo, hi, t;
   mpz_t z;
   int init;
 } Scratch;
@@ -447,6 +447,7 @@ static Scratch *scratch(void) {
     mpfr_init2(s->err, 64);
     mpfr_init2(s->lo, 168);
     mpfr_init2(s->hi, 168);
+    mpfr_init2(s->t, 224);
     mpz_init(s->z);
     s->init = 1;
   }
@@ -457,7 +458,7 @@ static void scratch_release(void) {
   Scratch *s = &tls;
   if (s->init) {
     mpfr_clear(s->x); mpfr_clear(s->v); mpfr_clear(s->err);
-    mpfr_clear(s->lo); mpfr_clear(s->hi); mpz_clear(s->z);
+    mpfr_clear(s->lo); mpfr_clear(s->hi); mpfr_clear(s->t); mpz_clear(s->z);
     mpfr_free_cache();
     s->init = 0;
   }
@@ -739,6 +740,148 @@ EXPORT int crvec_oracle_f64_all_modes(int f, uint64_t xbits, uint64_t out[4]) {
   return all_modes_f64(f, xbits, out);
 }
 
+
+
+/* ------------------------------------------ boundary distance / search --- */
+/* ref: proj/src/oracle.cpp:430-580 (consider_candidate, boundary_distance_f32/
+ * f64, hardest_case_search): distance of f(x) (160-bit evaluation) to the
+ * nearest rounding boundary (the RN result and the two flanking midpoints), in
+ * units of 2^-160; exact results are flagged, specials / saturated inputs are
+ * outside the domain. */
+static void consider_candidate(Scratch *s, double *best) {
+  mpfr_sub(s->t, s->v, s->t, MPFR_RNDN);
+  mpfr_abs(s->t, s->t, MPFR_RNDN);
+  mpfr_mul_2si(s->t, s->t, 160, MPFR_RNDN);
+  double d = mpfr_get_d(s->t, MPFR_RNDU);
+  if (d < *best) *best = d;
+}
+
+static int64_t ordered32(uint32_t b) {
+  int64_t mag = b & 0x7FFFFFFFu;
+  return (b >> 31) ? -mag - 1 : mag;
+}
+static uint32_t from_ordered32(int64_t o) {
+  if (o >= 0) return (uint32_t)o;
+  return 0x80000000u | (uint32_t)(-(o + 1));
+}
+
+EXPORT int crvec_oracle_boundary_distance_f32(int f, uint32_t xb, double *dist, int *exact,
+                                              int *domain) {
+  *dist = 0.0; *exact = 0; *domain = 1;
+  if ((xb & 0x7F800000u) == 0x7F800000u) { *domain = 0; return 0; }
+  double xd = (double)bitsf(xb);
+  if ((f == FN_LOG || f == FN_LOG2) && xd <= 0.0) { *domain = 0; return 0; }
+  Shortcut sc = shortcut_eval(f, xd, 1);
+  if (sc.kind == SC_PARTS && sc.value_exact) { *exact = 1; return 0; }
+  if (sc.kind != SC_NONE) { *domain = 0; return 0; }
+  Scratch *s = scratch();
+  mpfr_set_d(s->x, xd, MPFR_RNDN);
+  mpfr_set_prec(s->v, 160);
+  eval_into(s->v, f, s->x);
+  SigParts p = sig_parts_from(s->v, s->z);
+  int inexact;
+  uint32_t rn = round_sig_to_binary32(&p, RNE, &inexact);
+  if (!inexact) { *exact = 1; return 0; }
+  double best = INFINITY;
+  mpfr_set_prec(s->t, 224);
+  mpfr_set_d(s->t, (double)bitsf(rn), MPFR_RNDN);
+  consider_candidate(s, &best);
+  int64_t o = ordered32(rn);
+  for (int dir = -1; dir <= 1; dir += 2) {
+    uint32_t nb = from_ordered32(o + dir);
+    double nbv = ((nb & 0x7F800000u) == 0x7F800000u) ? (dir > 0 ? 0x1p128 : -0x1p128)
+                                                      : (double)bitsf(nb);
+    mpfr_set_prec(s->t, 224);
+    mpfr_set_d(s->t, (double)bitsf(rn), MPFR_RNDN);
+    mpfr_add_d(s->t, s->t, nbv, MPFR_RNDN);
+    mpfr_div_2si(s->t, s->t, 1, MPFR_RNDN);
+    consider_candidate(s, &best);
+  }
+  *dist = best;
+  return 0;
+}
+
+EXPORT int crvec_oracle_boundary_distance_f64(int f, uint64_t xbits, double *dist, int *exact,
+                                              int *domain) {
+  *dist = 0.0; *exact = 0; *domain = 1;
+  if (f != FN_EXP2 && f != FN_LOG && f != FN_LOG2) return -2;
+  double xd = bitsd(xbits);
+  if (!isfinite(xd)) { *domain = 0; return 0; }
+  if (f != FN_EXP2 && xd <= 0.0) { *domain = 0; return 0; }
+  Shortcut sc = shortcut_eval(f, xd, 0);
+  if (sc.kind == SC_PARTS && sc.value_exact) { *exact = 1; return 0; }
+  if (sc.kind != SC_NONE) { *domain = 0; return 0; }
+  Scratch *s = scratch();
+  mpfr_set_d(s->x, xd, MPFR_RNDN);
+  mpfr_set_prec(s->v, 160);
+  eval_into(s->v, f, s->x);
+  SigParts p = sig_parts_from(s->v, s->z);
+  int inexact;
+  uint64_t rn = round_sig_to_binary64(&p, RNE, &inexact);
+  if (!inexact) { *exact = 1; return 0; }
+  double best = INFINITY, rd = bitsd(rn);
+  mpfr_set_prec(s->t, 288);
+  mpfr_set_d(s->t, rd, MPFR_RNDN);
+  consider_candidate(s, &best);
+  for (int dir = -1; dir <= 1; dir += 2) {
+    uint64_t nb;
+    if ((rn << 1) == 0) {
+      nb = ((dir > 0) == ((rn >> 63) == 0)) ? 0x1ull : 0x8000000000000001ull;
+    } else {
+      int away = (dir > 0) == ((rn >> 63) == 0);
+      nb = rn + (away ? 1 : (uint64_t)-1);
+    }
+    mpfr_set_prec(s->t, 288);
+    mpfr_set_d(s->t, rd, MPFR_RNDN);
+    double nbd = bitsd(nb);
+    if (!isfinite(nbd)) {
+      mpfr_t big;
+      mpfr_init2(big, 64);
+      mpfr_set_ui_2exp(big, 1, 1024, MPFR_RNDN);
+      if (dir < 0) mpfr_neg(big, big, MPFR_RNDN);
+      mpfr_add(s->t, s->t, big, MPFR_RNDN);
+      mpfr_clear(big);
+    } else {
+      mpfr_add_d(s->t, s->t, nbd, MPFR_RNDN);
+    }
+    mpfr_div_2si(s->t, s->t, 1, MPFR_RNDN);
+    consider_candidate(s, &best);
+  }
+  *dist = best;
+  return 0;
+}
+
+typedef struct { uint32_t bits; double d; } HardCase;
+static int hc_cmp(const void *a, const void *b) {
+  const HardCase *x = (const HardCase *)a, *y = (const HardCase *)b;
+  if (x->d < y->d) return -1;
+  if (x->d > y->d) return 1;
+  return x->bits < y->bits ? -1 : (x->bits > y->bits);  /* stable: input order */
+}
+
+/* Every non-exact in-domain input in [lo, hi] ranked ascending by boundary
+ * distance; writes up to cap entries (cap 0 = all; buffers sized by caller
+ * via a first call with out == NULL). Returns the number of candidates. */
+EXPORT uint64_t crvec_oracle_hardest_case_search(int f, uint32_t lo, uint32_t hi, uint32_t *out_bits,
+                                                 double *out_dist, uint64_t cap) {
+  uint64_t n = (uint64_t)hi - lo + 1, k = 0;
+  HardCase *v = (HardCase *)malloc(sizeof(HardCase) * n);
+  for (uint64_t b = lo; b <= hi; ++b) {
+    double d;
+    int ex, dom;
+    crvec_oracle_boundary_distance_f32(f, (uint32_t)b, &d, &ex, &dom);
+    if (!dom || ex) continue;
+    v[k].bits = (uint32_t)b;
+    v[k].d = d;
+    ++k;
+  }
+  qsort(v, k, sizeof(HardCase), hc_cmp);
+  uint64_t m = (cap && cap < k) ? cap : k;
+  if (out_bits)
+    for (uint64_t i = 0; i < m; ++i) { out_bits[i] = v[i].bits; out_dist[i] = v[i].d; }
+  free(v);
+  return k;
+}
 
 /* ------------------------------------- independent MPFR-direct check ---- */
 /* Cross-check for the shortcut extension: f(x) correctly rounded by MPFR

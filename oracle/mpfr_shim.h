@@ -64,6 +64,8 @@ int mpfr_sub(mpfr_ptr, mpfr_srcptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_mul(mpfr_ptr, mpfr_srcptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_div(mpfr_ptr, mpfr_srcptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_mul_2si(mpfr_ptr, mpfr_srcptr, long, mpfr_rnd_t);
+int mpfr_div_2si(mpfr_ptr, mpfr_srcptr, long, mpfr_rnd_t);
+int mpfr_add_d(mpfr_ptr, mpfr_srcptr, double, mpfr_rnd_t);
 int mpfr_cmp(mpfr_srcptr, mpfr_srcptr);
 int mpfr_const_pi(mpfr_ptr, mpfr_rnd_t);
 void mpfr_free_cache(void);

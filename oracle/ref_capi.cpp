@@ -127,4 +127,32 @@ int crvec_ref_batch_f64(int f, const uint64_t* x, uint64_t* y, uint64_t n, int m
   return rc.load();
 }
 
+int crvec_ref_boundary_distance_f32(int f, uint32_t x, double *dist, int *exact, int *domain) {
+  auto d = boundary_distance_f32(static_cast<FuncId>(f), Binary32(x));
+  *dist = d.scaled_distance;
+  *exact = d.exact;
+  *domain = d.domain;
+  return 0;
+}
+
+int crvec_ref_boundary_distance_f64(int f, uint64_t x, double *dist, int *exact, int *domain) {
+  auto d = boundary_distance_f64(static_cast<FuncId>(f), Binary64(x));
+  *dist = d.scaled_distance;
+  *exact = d.exact;
+  *domain = d.domain;
+  return 0;
+}
+
+uint64_t crvec_ref_hardest_case_search(int f, uint32_t lo, uint32_t hi, uint32_t *out_bits,
+                                       double *out_dist, uint64_t cap) {
+  auto v = hardest_case_search(static_cast<FuncId>(f), lo, hi, 0);
+  uint64_t m = (cap && cap < v.size()) ? cap : v.size();
+  if (out_bits)
+    for (uint64_t i = 0; i < m; ++i) {
+      out_bits[i] = v[i].input_bits;
+      out_dist[i] = v[i].scaled_distance;
+    }
+  return v.size();
+}
+
 }  // extern "C"

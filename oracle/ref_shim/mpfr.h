@@ -6,8 +6,6 @@
 #include <climits>
 #include "../mpfr_shim.h"
 extern "C" {
-int mpfr_add_d(mpfr_ptr, mpfr_srcptr, double, mpfr_rnd_t);
-int mpfr_div_2si(mpfr_ptr, mpfr_srcptr, long, mpfr_rnd_t);
 int mpfr_cmp_d(mpfr_srcptr, double);
 int mpfr_cmp_ui_2exp(mpfr_srcptr, unsigned long, mpfr_exp_t);
 int mpfr_sub_ui(mpfr_ptr, mpfr_srcptr, unsigned long, mpfr_rnd_t);

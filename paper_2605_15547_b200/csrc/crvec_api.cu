@@ -287,6 +287,22 @@ int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_
   return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
 }
 
+// ---- hard-case screen ----
+int crvec_hardcase_scan_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, double rel_threshold,
+                            uint32_t *out_bits, double *out_dist, uint64_t capacity,
+                            uint64_t *count, void *stream) {
+  if (fn < 0 || fn >= CRVEC_FN_COUNT || fn == CRVEC_FN_SINCOSF || chunk_hi > 4096 ||
+      chunk_lo >= chunk_hi || !count || (capacity && (!out_bits || !out_dist)))
+    return CRVEC_EINVAL;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  cudaError_t e = g_table[fn].scan(chunk_lo, chunk_hi, rel_threshold, out_bits, out_dist,
+                                   (unsigned long long)capacity, (unsigned long long *)count,
+                                   (cudaStream_t)stream);
+  return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
 // ---- accounting ----
 int crvec_stats_get(crvec_stats_t *out) {
   if (!out) return CRVEC_EINVAL;

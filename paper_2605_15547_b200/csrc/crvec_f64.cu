@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kT64) k_f64(const double *x, double *y, uint64
     T.t3h[i] = EXP2D_T3_HI[i]; T.t3l[i] = EXP2D_T3_LO[i];
   }
   for (int i = threadIdx.x; i < 128; i += kT64) {
-    T.lc[i] = LOGD_C[i]; T.llh[i] = LOGD_L_HI[i]; T.lll[i] = LOGD_L_LO[i];
+    T.lc[i] = LOGD_C[i]; T.llh[i] = LOGD_LT_HI[i]; T.lll[i] = LOGD_LT_LO[i];
   }
   __syncthreads();
   F64Queue &q = Q[threadIdx.x >> 5];
@@ -62,19 +62,28 @@ __global__ void __launch_bounds__(kT64) k_f64(const double *x, double *y, uint64
   const uint64_t nwarps = ((uint64_t)gridDim.x * kT64) >> 5;
   const uint64_t n2 = (n + 1) / 2;  // double2 slots
   const bool vec = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
-  for (uint64_t base = warp * 32; base < n2; base += nwarps * 32) {
+  // register double buffer: the next slot's two doubles are requested before
+  // this slot is computed
+  auto load2 = [&](uint64_t slot) {
+    uint64_t j = 2 * slot;
+    double2 t = make_double2(1.0, 1.0);
+    if (vec && j + 1 < n) {
+      t = __ldcs((const double2 *)(x + j));
+    } else {
+      if (j < n) t.x = x[j];
+      if (j + 1 < n) t.y = x[j + 1];
+    }
+    return t;
+  };
+  const uint64_t stride = nwarps * 32;
+  double2 cur = load2(warp * 32 + lane);
+  for (uint64_t base = warp * 32; base < n2; base += stride) {
     uint64_t s = base + lane;
     uint64_t i0 = 2 * s;
-    double xv[2] = {1.0, 1.0};
+    double2 nxt = load2(s + stride);
+    double xv[2] = {cur.x, cur.y};
+    cur = nxt;
     bool v0 = i0 < n, v1 = i0 + 1 < n;
-    if (vec && v1) {
-      double2 t = __ldcs((const double2 *)(x + i0));
-      xv[0] = t.x;
-      xv[1] = t.y;
-    } else {
-      if (v0) xv[0] = x[i0];
-      if (v1) xv[1] = x[i0 + 1];
-    }
     F64Out r[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e)

@@ -6,6 +6,6 @@ void register_trig(FnEntry *t) {
   t[9] = make_entry<FnCos>();
   t[10] = make_entry<FnTan>();
   t[18] = FnEntry{{launch_sincos<RNE>, launch_sincos<RZ>, launch_sincos<RU>, launch_sincos<RD>},
-                  launch_sweep_sincos};
+                  launch_sweep_sincos, nullptr};
 }
 }  // namespace crvec

@@ -287,7 +287,7 @@ CR_F double logd_accurate(double x, int *undecided) {
 // --------------------------------------------------------- fast paths ----
 struct F64Tab {
   double t1h[16], t1l[16], t2h[16], t2l[16], t3h[16], t3l[16];
-  double lc[128], llh[128], lll[128];
+  double lc[128], llh[128], lll[128];  // llh: -log(c_i) on the 2^-40 grid
 };
 
 struct F64Out {
@@ -322,7 +322,7 @@ CR_F F64Out round_test64(double h, double l, double b) {
 }
 
 constexpr double EPS_EXP2D = 0x1p-74;
-constexpr double EPS_LOGD = 0x1p-73;
+constexpr double EPS_LOGD = 0x1p-73;  // error analysis: < 2^-76
 
 template <int M>
 CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
@@ -354,12 +354,15 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
   double q = fma_(fma_(fma_(fma_(EXP2D_Q[5], R, EXP2D_Q[4]), R, EXP2D_Q[3]), R, EXP2D_Q[2]), R,
                   EXP2D_Q[1]);
   q = fma_(q, R, EXP2D_Q[0]);
+  // 2^R = 1 + p, p = ph + pl: ph = RN(R ln2_hi) with its exact error folded
+  // into pl together with R ln2_lo and R^2 q(R) (|pl| ~ 2^-53 |p|).
   DD lin = two_prod(R, LN2D_H);
-  DD s = fast_two_sum(1.0, lin.hi);
-  double lo = add_(add_(s.lo, lin.lo), fma_(R, LN2D_L, mul_(mul_(R, R), q)));
-  DD P = fast_two_sum(s.hi, lo);
-  DD V = dd_mul(Tv, P);
-  V = fast_two_sum(V.hi, V.lo);
+  double pl = add_(lin.lo, fma_(R, LN2D_L, mul_(mul_(R, R), q)));
+  // V = T (1 + p) = T.hi + T.hi ph + [T.lo + T.hi pl + T.lo ph], T.hi ph exact
+  DD a = two_prod(Tv.hi, lin.hi);
+  DD v = fast_two_sum(Tv.hi, a.hi);
+  double lo = add_(add_(v.lo, a.lo), fma_(Tv.hi, pl, fma_(Tv.lo, lin.hi, Tv.lo)));
+  DD V = fast_two_sum(v.hi, lo);
   F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
   if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
   // scale by 2^N (exact for normal results; 2^1024 overflow only when rounding to 2)
@@ -387,25 +390,26 @@ CR_F F64Out logd_fast(double x, const F64Tab &T) {
   int e = (hh >> 20) + eadj;
   int i = (hh >> 13) & 127;
   double m = hilo2d(h - ((hh >> 20) << 20), d2lo(xs));
-  double c = T.lc[i];
-  DD pm = two_prod(m, c);
-  DD r = fast_two_sum(sub_(pm.hi, 1.0), pm.lo);  // r = m c - 1 exactly
-  double rh = r.hi, rl = r.lo;
-  DD sq = two_prod(rh, rh);
-  DD b = {-0.5 * sq.hi, -0.5 * sq.lo};             // -rh^2/2 (exact)
-  DD cube = dd_mul_d(sq, rh);                       // rh^3
-  DD c3 = dd_mul(cube, DD{THIRD_H, THIRD_L});       // rh^3/3
+  // r = m c - 1 is exact: c has 7 significant bits, m 53, |r| < 2^-7
+  // (ref: proj/src/kernels_f64.cpp:298-300, "exact or near-exact by construction")
+  double r = fma_(m, T.lc[i], -1.0);
+  DD s = two_prod(r, r);                       // r^2 exact
+  DD u = two_prod(r, s.hi);                    // r^3 ~ u.hi + (u.lo + r s.lo)
+  double ul = fma_(r, s.lo, u.lo);
+  double c3h = mul_(u.hi, THIRD_H);            // r^3 / 3 as c3h + c3l (~2^-100)
+  double c3l = fma_(u.hi, THIRD_H, -c3h) + fma_(ul, THIRD_H, mul_(u.hi, THIRD_L));
   double qt = LOGD_TAIL[8];
-  for (int n = 7; n >= 0; --n) qt = fma_(qt, rh, LOGD_TAIL[n]);
-  double rest = mul_(mul_(sq.hi, sq.hi), qt);       // rh^4 (-1/4 + rh/5 - ...)
-  double corr = mul_(rl, fma_(rh, sub_(rh, 1.0), 1.0));  // rl (1 - rh + rh^2)
-  DD u = fast_two_sum(rh, b.hi);
-  double small = add_(add_(add_(add_(u.lo, b.lo), c3.hi), add_(rest, corr)), c3.lo);
-  DD P = fast_two_sum(u.hi, small);
+  for (int n = 7; n >= 0; --n) qt = fma_(qt, r, LOGD_TAIL[n]);
+  double tail = mul_(mul_(s.hi, s.hi), qt);    // r^4 (-1/4 + r/5 - ...), rel 2^-52
+  DD a = fast_two_sum(r, -0.5 * s.hi);         // |r| > |r^2/2|
+  DD b = fast_two_sum(a.hi, c3h);
+  double small = add_(add_(a.lo, b.lo), add_(fma_(-0.5, s.lo, c3l), tail));
+  // e ln2 + L: the high parts add exactly (both on the 2^-40 grid)
   double ed = i2d(e);
-  DD el = two_sum(mul_(ed, LN2_H), mul_(ed, LN2_M));
-  el = dd_add_d(el, mul_(ed, LN2_L));
-  DD V = dd_add(dd_add(el, DD{T.llh[i], T.lll[i]}), P);
+  double th = fma_(ed, LN2_HD, T.llh[i]);
+  double tl = fma_(ed, LN2_LD, T.lll[i]);
+  DD v = two_sum(th, b.hi);
+  DD V = fast_two_sum(v.hi, add_(add_(v.lo, tl), small));
   return round_test64<M>(V.hi, V.lo, EPS_LOGD * dabs(V.hi));
 }
 

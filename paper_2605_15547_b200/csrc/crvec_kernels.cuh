@@ -168,34 +168,52 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // ------------------------------------------------------------ map kernels ----
 // 4 elements (one float4) per lane per iteration; the loop trip count is
 // warp-uniform so the register-table shuffles always see a full warp.
+// Float4s per lane per iteration (8 elements per lane): measured best for
+// every family incl. trig (tools/membench.cu, profiles/r01).
+template <class F>
+struct VecWidth {
+  static constexpr int value = 2;
+};
+
 template <class F, int M>
 __global__ void __launch_bounds__(kThreads) k_map_vec(const float4 *x, float4 *y, uint64_t n4,
                                                       unsigned long long *counters) {
+  constexpr int NV = VecWidth<F>::value;
   PHBlock *sh = ph_storage<F>();
   typename F::Regs R;
   F::load(R);
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  // Each warp handles 2 x 32 float4 per iteration (8 elements per lane) and
-  // requests the next iteration's two float4 before computing this one
-  // (register double buffer): four 16-byte loads in flight per lane.
-  const uint64_t stride = nwarps * 64;
+  // Each warp handles NV x 32 float4 per iteration and requests the next
+  // iteration's float4s before computing this one (register double buffer).
+  const uint64_t stride = nwarps * 32 * NV;
   const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
-  uint64_t base = warp * 64;
-  float4 v0 = base + lane < n4 ? ld_stream(x + base + lane) : ones;
-  float4 v1 = base + 32 + lane < n4 ? ld_stream(x + base + 32 + lane) : ones;
+  uint64_t base = warp * 32 * NV;
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = base + 32 * k + lane < n4 ? ld_stream(x + base + 32 * k + lane) : ones;
   for (; base < n4; base += stride) {
-    uint64_t i0 = base + lane, i1 = i0 + 32;
-    float4 n0 = i0 + stride < n4 ? ld_stream(x + i0 + stride) : ones;
-    float4 n1 = i1 + stride < n4 ? ld_stream(x + i1 + stride) : ones;
-    float xs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    uint32_t ys[8];
-    eval_lanes<F, M, 8>(xs, ys, R, sh, counters);
-    if (i0 < n4) st_stream(y + i0, make_float4(u2f(ys[0]), u2f(ys[1]), u2f(ys[2]), u2f(ys[3])));
-    if (i1 < n4) st_stream(y + i1, make_float4(u2f(ys[4]), u2f(ys[5]), u2f(ys[6]), u2f(ys[7])));
-    v0 = n0;
-    v1 = n1;
+    float4 nx[NV];
+    float xs[4 * NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t in = base + 32 * k + lane + stride;
+      nx[k] = in < n4 ? ld_stream(x + in) : ones;
+      xs[4 * k] = v[k].x;
+      xs[4 * k + 1] = v[k].y;
+      xs[4 * k + 2] = v[k].z;
+      xs[4 * k + 3] = v[k].w;
+    }
+    uint32_t ys[4 * NV];
+    eval_lanes<F, M, 4 * NV>(xs, ys, R, sh, counters);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t i = base + 32 * k + lane;
+      if (i < n4)
+        st_stream(y + i, make_float4(u2f(ys[4 * k]), u2f(ys[4 * k + 1]), u2f(ys[4 * k + 2]), u2f(ys[4 * k + 3])));
+      v[k] = nx[k];
+    }
   }
 }
 
@@ -454,6 +472,62 @@ __global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, ui
   block_add<4>(c4, hc + 4ull * (chunk - chunk_lo));
 }
 
+
+// ------------------------------------------------------- hard-case screen ----
+// GPU worst-case finder (the reference's hardest_case_search,
+// ref: proj/src/oracle.cpp:565-580, is a CPU loop over MPFR): every pattern of
+// the chunk range is evaluated on the double-double path and its relative
+// distance to the nearest binary32 rounding boundary (representable value or
+// midpoint, any mode) is measured; inputs closer than 2^-thr are appended.
+__device__ __forceinline__ double boundary_rel_distance(DD v) {
+  double h = v.hi;
+  if (!(dabs(h) < 0x1p128) || h == 0.0) return 1.0;
+  uint64_t b = d2u(h);
+  uint64_t q = (b + (1ull << 27)) & ~((1ull << 28) - 1);  // nearest 25-bit lattice point
+  double dq = u2d(q);
+  double d = add_(sub_(h, dq), v.lo);  // h - dq exact (same or adjacent binade)
+  return dabs(d) / dabs(h);
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_hardscan(uint32_t chunk_lo, double thr,
+                                                       uint32_t *out_bits, double *out_dist,
+                                                       unsigned long long cap,
+                                                       unsigned long long *count) {
+  typename F::Regs R;
+  F::load(R);
+  uint32_t chunk = chunk_lo + blockIdx.x / kSweepBlocksPerChunk;
+  uint32_t p0 = (chunk << 20) + (blockIdx.x % kSweepBlocksPerChunk) * kSweepPerBlock;
+#pragma unroll 1
+  for (int it = 0; it < kSweepPerThread; ++it) {
+    uint32_t xb = p0 + it * kThreads + threadIdx.x;
+    float x = u2f(xb);
+    Fast f;
+    if constexpr (IsTrig<F>::value) f = F::from_red(x, RedTrig{0, 0.0}, R);  // only .main is used
+    else f = F::fast(x, R);
+    if (f.main) {  // divergent body without shuffles; fast() above runs converged
+      double d = boundary_rel_distance(slow_dd<F>(x));
+      if (d < thr) {
+        unsigned long long k = atomicAdd(count, 1ull);
+        if (k < cap) {
+          out_bits[k] = xb;
+          out_dist[k] = d;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <class F>
+cudaError_t launch_hardscan(uint32_t chunk_lo, uint32_t chunk_hi, double thr, uint32_t *bits,
+                            double *dist, unsigned long long cap, unsigned long long *count,
+                            cudaStream_t s) {
+  unsigned blocks = (chunk_hi - chunk_lo) * kSweepBlocksPerChunk;
+  k_hardscan<F><<<blocks, kThreads, 0, s>>>(chunk_lo, thr, bits, dist, cap, count);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- launchers ----
 using MapLaunch = cudaError_t (*)(const float *, float *, float *, uint64_t, cudaStream_t,
                                   unsigned long long *);
@@ -485,7 +559,7 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
   bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
   uint64_t n4 = aligned ? n / 4 : 0;
   if (n4) {
-    k_map_vec<F, M><<<grid_for((n4 + 63) / 64, mb_vec), kThreads, 0, s>>>(
+    k_map_vec<F, M><<<grid_for((n4 + 32 * VecWidth<F>::value - 1) / (32 * VecWidth<F>::value), mb_vec), kThreads, 0, s>>>(
         (const float4 *)x, (float4 *)y, n4, ctr);
   }
   uint64_t rem = n - 4 * n4;
@@ -532,14 +606,17 @@ inline cudaError_t launch_sweep_sincos(uint32_t chunk_lo, uint32_t chunk_hi, uin
 }
 
 // Registration: each family translation unit fills its rows.
+using ScanLaunch = cudaError_t (*)(uint32_t, uint32_t, double, uint32_t *, double *,
+                                   unsigned long long, unsigned long long *, cudaStream_t);
 struct FnEntry {
   MapLaunch map[4];
   SweepLaunch sweep;
+  ScanLaunch scan;
 };
 template <class F>
 constexpr FnEntry make_entry() {
   return FnEntry{{launch_map<F, RNE>, launch_map<F, RZ>, launch_map<F, RU>, launch_map<F, RD>},
-                 launch_sweep<F>};
+                 launch_sweep<F>, launch_hardscan<F>};
 }
 
 }  // namespace crvec

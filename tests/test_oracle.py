@@ -191,3 +191,59 @@ def test_sweep_hash_definition(oracle):
         h = oracle.mix64((y[:, m].astype(np.uint64) << np.uint64(32)) | p.astype(np.uint64))
         want = oracle.sweep_hashes("exp", 1000, 1001)[0, m]
         assert np.uint64(h.sum(dtype=np.uint64)) == want
+
+
+def _bd(lib, fname, f, x):
+    d, ex, dom = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    getattr(lib, fname)(f, x, ctypes.byref(d), ctypes.byref(ex), ctypes.byref(dom))
+    return d.value, ex.value, dom.value
+
+
+def test_boundary_distance_and_hardest_case_search_match_reference(ref_oracle):
+    """ref: proj/src/oracle.cpp:430-580; ref test proj/tests/test_oracle.cpp:221-246."""
+    O = ref_oracle
+    L, R = O.lib(), O.ref()
+    for lib in (L, R):
+        pfx = "crvec_oracle_" if lib is L else "crvec_ref_"
+        getattr(lib, pfx + "boundary_distance_f32").argtypes = [ctypes.c_int, ctypes.c_uint32] + [ctypes.c_void_p] * 3
+        getattr(lib, pfx + "boundary_distance_f64").argtypes = [ctypes.c_int, ctypes.c_uint64] + [ctypes.c_void_p] * 3
+        getattr(lib, pfx + "hardest_case_search").restype = ctypes.c_uint64
+        getattr(lib, pfx + "hardest_case_search").argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
+    rng = np.random.default_rng(42)
+    xs = rng.integers(0, 2 ** 32, 3000, dtype=np.uint64).astype(np.uint32)
+    for fn in O.REF_FNS:
+        f = O.FN[fn]
+        for x in xs:
+            assert _bd(L, "crvec_oracle_boundary_distance_f32", f, int(x)) == \
+                _bd(R, "crvec_ref_boundary_distance_f32", f, int(x)), (fn, hex(int(x)))
+    x64 = rng.integers(0, 2 ** 64, 1500, dtype=np.uint64)
+    for fn in ("exp2", "log"):
+        f = O.FN[fn]
+        for x in x64:
+            assert _bd(L, "crvec_oracle_boundary_distance_f64", f, int(x)) == \
+                _bd(R, "crvec_ref_boundary_distance_f64", f, int(x)), (fn, hex(int(x)))
+    lo, hi = f2u(1.0), f2u(1.0 + 2.0 ** -10)
+    res = []
+    for lib, pfx in ((L, "crvec_oracle_"), (R, "crvec_ref_")):
+        n = getattr(lib, pfx + "hardest_case_search")(O.FN["exp2"], lo, hi, None, None, 0)
+        bits, dist = np.zeros(n, np.uint32), np.zeros(n, np.float64)
+        getattr(lib, pfx + "hardest_case_search")(O.FN["exp2"], lo, hi, bits.ctypes.data, dist.ctypes.data, 0)
+        res.append((bits, dist))
+    assert (res[0][0] == res[1][0]).all() and (res[0][1] == res[1][1]).all()
+    assert (np.diff(res[0][1]) >= 0).all()
+    assert _bd(L, "crvec_oracle_boundary_distance_f32", O.FN["log2"], f2u(4.0))[1] == 1  # exact
+
+
+def test_hardcase_corpus_expected_outputs(oracle):
+    """Expected outputs stored in the hard-case corpus equal the oracle's."""
+    d = os.path.join(ROOT, "tests", "golden", "hardcases")
+    if not os.path.isdir(d):
+        pytest.skip("no hard-case corpus yet")
+    import paper_2605_15547_b200 as crvec
+    for f in sorted(os.listdir(d)):
+        name = f[:-4]
+        rows = [l.split() for l in open(os.path.join(d, f)) if l.strip() and not l.startswith("#")]
+        x = np.array([int(r[0], 16) for r in rows], np.uint32)
+        want = np.array([[int(v, 16) for v in r[3:7]] for r in rows], np.uint32)
+        assert (oracle.f32(crvec.ORACLE_NAME[name], x, None, use_ld=False) == want).all(), name

@@ -11,7 +11,7 @@ static void init() {
   std::memcpy(T.t1h, EXP2D_T1_HI, 128); std::memcpy(T.t1l, EXP2D_T1_LO, 128);
   std::memcpy(T.t2h, EXP2D_T2_HI, 128); std::memcpy(T.t2l, EXP2D_T2_LO, 128);
   std::memcpy(T.t3h, EXP2D_T3_HI, 128); std::memcpy(T.t3l, EXP2D_T3_LO, 128);
-  std::memcpy(T.lc, LOGD_C, 1024); std::memcpy(T.llh, LOGD_L_HI, 1024); std::memcpy(T.lll, LOGD_L_LO, 1024);
+  std::memcpy(T.lc, LOGD_C, 1024); std::memcpy(T.llh, LOGD_LT_HI, 1024); std::memcpy(T.lll, LOGD_LT_LO, 1024);
   done = true;
 }
 template <int M>

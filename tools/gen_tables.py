@@ -315,6 +315,13 @@ def gen_f64():
     arr("LOGD_C", cs)
     arr("LOGD_L_HI", [dd(v)[0] for v in Ls])
     arr("LOGD_L_LO", [dd(v)[1] for v in Ls])
+    # L_i trimmed to the 2^-40 grid so e*LN2_H + L_i is exact in one add
+    Lt = [mp.nint(v * mp.mpf(2) ** 40) / mp.mpf(2) ** 40 for v in Ls]
+    arr("LOGD_LT_HI", [d(v) for v in Lt])
+    arr("LOGD_LT_LO", [d(v - t) for v, t in zip(Ls, Lt)])
+    h, m, l = split3(LN2, 40, 40)
+    scalar("LN2_HD", h)
+    scalar("LN2_LD", d(LN2 - h))
     arr("LOGD_TAIL", [d(mp.mpf((-1) ** (n + 1)) / n) for n in range(4, 13)])
     h, l = dd(mp.mpf(1) / 3)
     scalar("THIRD_H", h); scalar("THIRD_L", l)

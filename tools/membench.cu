@@ -17,11 +17,9 @@ struct FnIdent {
   static constexpr uint32_t E = 8;
   struct Regs {};
   CR_F static void load(Regs &) {}
-  CR_F static Fast fast(float x, const Regs &) {
-    Fast f = fast_of(f2d(x));
-    f.skip = true;
-    return f;
-  }
+  CR_F static Fast fast(float x, const Regs &) { return Fast{f2d(x), false}; }
+  template <int M>
+  CR_F static uint32_t special(float x) { return f2u(x); }
   CR_F static DD slow(float x) { return DD{f2d(x), 0.0}; }
 };
 
@@ -65,6 +63,41 @@ __global__ void __launch_bounds__(256) k_var(const float4 *x, float4 *y, uint64_
     if (PF) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) v[k] = vn[k];
+    }
+  }
+}
+
+template <class F, int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_lb(const float4 *x, float4 *y, uint64_t n4,
+                                                  unsigned long long *ctr) {
+  typename F::Regs R;
+  F::load(R);
+  PHBlock *sh = ph_storage<F>();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * 256) >> 5;
+  const uint64_t stride = nwarps * 32 * NV;
+  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
+  uint64_t base = warp * 32 * NV;
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = base + 32 * k + lane < n4 ? ld_stream(x + base + 32 * k + lane) : ones;
+  for (; base < n4; base += stride) {
+    float4 nx[NV];
+    float xs[4 * NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t in = base + 32 * k + lane + stride;
+      nx[k] = in < n4 ? ld_stream(x + in) : ones;
+      xs[4 * k] = v[k].x; xs[4 * k + 1] = v[k].y; xs[4 * k + 2] = v[k].z; xs[4 * k + 3] = v[k].w;
+    }
+    uint32_t ys[4 * NV];
+    eval_lanes<F, RNE, 4 * NV>(xs, ys, R, sh, ctr);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t i = base + 32 * k + lane;
+      if (i < n4) st_stream(y + i, make_float4(u2f(ys[4 * k]), u2f(ys[4 * k + 1]), u2f(ys[4 * k + 2]), u2f(ys[4 * k + 3])));
+      v[k] = nx[k];
     }
   }
 }
@@ -194,31 +227,19 @@ int main() {
       rep(nm, timeit(k, sms * per * mult, x4, y4, n4, c), per);                      \
     }                                                                                \
   }
-  RUNV(FnIdent, 1, true)
-  RUNV(FnIdent, 1, false)
-  RUNV(FnIdent, 2, false)
-  RUNV(FnIdent, 2, true)
-  RUNV(FnLog, 1, true)
-  RUNV(FnLog, 2, false)
-  RUNV(FnLog, 2, true)
-  RUNV(FnExp, 1, true)
-  RUNV(FnExp, 2, true)
-  RUNV(FnRsqrt, 1, true)
-  RUNV(FnRsqrt, 2, true)
-  {
-    auto k = k_tma<FnIdent, 4>;
-    int per = occ(k);
-    rep("TMA ident ST=4", timeit(k, sms * per, x4, y4, n4, c), per);
-    auto k8 = k_tma<FnIdent, 8>;
-    per = occ(k8);
-    rep("TMA ident ST=8", timeit(k8, sms * per, x4, y4, n4, c), per);
-    auto kl = k_tma<FnLog, 4>;
-    per = occ(kl);
-    rep("TMA logf ST=4", timeit(kl, sms * per, x4, y4, n4, c), per);
-    auto kl8 = k_tma<FnLog, 8>;
-    per = occ(kl8);
-    rep("TMA logf ST=8", timeit(kl8, sms * per, x4, y4, n4, c), per);
+#define RUNLB(F, NV, MB)                                                             \
+  {                                                                                  \
+    auto k = k_lb<F, NV, MB>;                                                        \
+    int per = occ(k);                                                                \
+    char nm[64];                                                                     \
+    snprintf(nm, 64, #F " NV=%d minB=%d", NV, MB);                                   \
+    rep(nm, timeit(k, sms * per * 4, x4, y4, n4, c), per);                           \
   }
+  RUNLB(FnLog, 2, 1) RUNLB(FnLog, 2, 3) RUNLB(FnLog, 2, 4) RUNLB(FnLog, 1, 4) RUNLB(FnLog, 1, 5) RUNLB(FnLog, 3, 2) RUNLB(FnLog, 3, 3)
+  RUNLB(FnLog1p, 2, 1) RUNLB(FnLog1p, 2, 3) RUNLB(FnLog1p, 2, 4) RUNLB(FnLog1p, 1, 4)
+  RUNLB(FnExp, 2, 1) RUNLB(FnExp, 2, 3) RUNLB(FnExp, 2, 4) RUNLB(FnExp, 1, 4)
+  RUNLB(FnSin, 2, 1) RUNLB(FnSin, 2, 2) RUNLB(FnSin, 2, 3) RUNLB(FnSin, 1, 4)
+  RUNLB(FnAsin, 2, 1) RUNLB(FnAsin, 2, 3) RUNLB(FnAsin, 1, 4)
   // plain cudaMemcpy D2D for reference
   {
     cudaEvent_t a, b;
