@@ -210,6 +210,63 @@ def run_sweep(rank, world, fns):
     return secs, mism, checked
 
 
+def all_functions_table(n=1 << 28, reps=5):
+    """Device throughput of every binary32 function (and the binary64 pair) at
+    2^28 (2^26 for binary64), inputs generated on the device: the configs'
+    distributions for the log and trig families, uniform over each function's
+    interesting range otherwise. Median of `reps` event-timed launches."""
+    import ctypes
+    import torch
+    import paper_2605_15547_b200 as crvec
+    from tests.inputs import RANGES
+    peak, _ = peaks()
+    L = crvec.lib()
+    s = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    y2 = torch.empty(n, dtype=torch.float32, device="cuda")
+    out = {}
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        return float(np.median(ts))
+
+    for name in crvec.F32_FUNCS + ["sincosf"]:
+        lo, hi = RANGES[name]
+        x = torch.rand(n, device="cuda", generator=g, dtype=torch.float32) * (hi - lo) + lo
+        if name in ("sinf", "cosf", "tanf", "sincosf"):  # config C3: 1/8 large-argument tail
+            big = torch.randint(0, 8, (n,), device="cuda", generator=g) == 0
+            e = torch.randint(142, 255, (n,), device="cuda", generator=g, dtype=torch.int32)
+            m = torch.randint(0, 1 << 23, (n,), device="cuda", generator=g, dtype=torch.int32)
+            sgn = torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int32) << 31
+            xb = (sgn | (e << 23) | m).view(torch.float32)
+            x = torch.where(big, xb, x)
+        fid = crvec.FN_IDS[name]
+        t = timed(lambda: L.crvec_eval_f32_dev(fid, x.data_ptr(), y.data_ptr(), y2.data_ptr(), n, 0, sp))
+        bpe = 12 if name == "sincosf" else 8
+        out[name] = {"gelem_s": round(n / t / 1e9, 1), "frac_hbm": round(bpe * n / t / 1e9 / peak, 3)}
+        del x
+    n64 = 1 << 26
+    for name, lo, hi in (("exp2", -20.0, 20.0), ("log", 0.125, 8.0)):
+        x = torch.rand(n64, device="cuda", generator=g, dtype=torch.float64) * (hi - lo) + lo
+        yy = torch.empty_like(x)
+        f = getattr(L, f"crvec_{name}_dev")
+        t = timed(lambda: f(x.data_ptr(), yy.data_ptr(), n64, 0, sp))
+        out[name + "(f64)"] = {"gelem_s": round(n64 / t / 1e9, 1), "frac_hbm": round(16 * n64 / t / 1e9 / peak, 3)}
+    return out
+
+
 # --------------------------------------------------------------- our arm -----
 def run_crvec(args, rank, world, local):
     import ctypes
@@ -292,6 +349,8 @@ def run_crvec(args, rank, world, local):
                  "mismatching_chunks": mism, "golden_sets_checked": checked, "ranks": world,
                  "collective": "one NCCL all_reduce of 20x4096x4 u64 chunk hashes" if world > 1 else None}
 
+    table = all_functions_table() if (rank == 0 and not args.no_table) else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, kind, dt = cpu_reference("log", args.cpu_sample)
@@ -318,6 +377,7 @@ def run_crvec(args, rank, world, local):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "sweep": sweep,
+            "functions": table,
         }
         print(json.dumps(line), flush=True)
 
@@ -331,6 +391,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-table", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))

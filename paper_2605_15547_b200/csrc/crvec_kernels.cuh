@@ -51,12 +51,11 @@ __device__ __noinline__ DD slow_dd(float x) {
 
 // ---------------------------------------------- warp-cooperative Payne-Hanek
 // Per-warp staging: the big-argument elements of the warp's 32 x NE slots are
-// compacted (ballot + popc prefix) into a queue, reduced 32 at a time by all
-// lanes, and scattered back. One pass serves up to 32 big arguments however
+// compacted (warp prefix sum of per-lane counts) into a queue, reduced 32 at
+// a time by all lanes, and read back by their owners. One pass serves up to 32 big arguments however
 // they are spread over lanes and slots.
 struct PHWarp {
   float qx[256];
-  unsigned short qslot[256];
   int rk[256];
   double rr[256];
 };
@@ -70,32 +69,40 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
                                                  RedTrig (&q)[NE], PHBlock &sh) {
   const int lane = threadIdx.x & 31;
   PHWarp &w = sh.warp[threadIdx.x >> 5];
-  const unsigned lt = (1u << lane) - 1u;
-  int total = 0;
+  // queue offsets: exclusive warp prefix sum of each lane's big-argument count
+  int nloc = 0;
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    unsigned m = __ballot_sync(kFull, big[e]);
-    if (big[e]) {
-      int pos = total + __popc(m & lt);
-      w.qx[pos] = xs[e];
-      w.qslot[pos] = (unsigned short)(e * 32 + lane);
-    }
-    total += __popc(m);
+  for (int e = 0; e < NE; ++e) nloc += big[e];
+  int incl = nloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
   }
-  __syncwarp();
-  for (int base = 0; base < total; base += 32) {
-    int i = base + lane;
-    if (i < total) {
-      RedTrig r = ph_reduce(w.qx[i], sh.words);
-      int s = w.qslot[i];
-      w.rk[s] = r.k;
-      w.rr[s] = r.r;
-    }
-  }
-  __syncwarp();
+  const int total = __shfl_sync(kFull, incl, 31);
+  const int base = incl - nloc;
+  int j = base;
 #pragma unroll
   for (int e = 0; e < NE; ++e)
-    if (big[e]) q[e] = RedTrig{w.rk[e * 32 + lane], w.rr[e * 32 + lane]};
+    if (big[e]) w.qx[j++] = xs[e];
+  __syncwarp();
+  // all lanes reduce the compacted queue, 32 arguments per pass
+  for (int b0 = 0; b0 < total; b0 += 32) {
+    int i = b0 + lane;
+    if (i < total) {
+      RedTrig r = ph_reduce(w.qx[i], sh.words);
+      w.rk[i] = r.k;
+      w.rr[i] = r.r;
+    }
+  }
+  __syncwarp();
+  j = base;
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+    if (big[e]) {
+      q[e] = RedTrig{w.rk[j], w.rr[j]};
+      ++j;
+    }
   __syncwarp();
 }
 
@@ -168,15 +175,32 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // ------------------------------------------------------------ map kernels ----
 // 4 elements (one float4) per lane per iteration; the loop trip count is
 // warp-uniform so the register-table shuffles always see a full warp.
-// Float4s per lane per iteration (8 elements per lane): measured best for
-// every family incl. trig (tools/membench.cu, profiles/r01).
+// Kernel shape per function, chosen by measurement (tools/membench.cu,
+// profiles/r01/membench2.txt): float4s per lane per iteration (NV) and the
+// __launch_bounds__ min-blocks register cap (MINB).
+template <class F>
+struct KernelShape {
+  static constexpr int nv = 2, minb = 3;
+};
+template <>
+struct KernelShape<FnLog1p> {
+  static constexpr int nv = 2, minb = 1;
+};
+template <int W>
+struct KernelShape<FnTrig<W>> {
+  static constexpr int nv = 2, minb = 2;
+};
+template <bool A>
+struct KernelShape<FnAsinAcos<A>> {
+  static constexpr int nv = 1, minb = 4;
+};
 template <class F>
 struct VecWidth {
-  static constexpr int value = 2;
+  static constexpr int value = KernelShape<F>::nv;
 };
 
 template <class F, int M>
-__global__ void __launch_bounds__(kThreads) k_map_vec(const float4 *x, float4 *y, uint64_t n4,
+__global__ void __launch_bounds__(kThreads, KernelShape<F>::minb) k_map_vec(const float4 *x, float4 *y, uint64_t n4,
                                                       unsigned long long *counters) {
   constexpr int NV = VecWidth<F>::value;
   PHBlock *sh = ph_storage<F>();

@@ -61,6 +61,8 @@ def main():
         t0 = time.time()
         bits, dist, total = scan(name, a.thr)
         t1 = time.time() - t0
+        keep = dist > 0  # distance 0: algebraically exact results (2^k, log2(2^k)), not hard cases
+        bits, dist = bits[keep], dist[keep]
         order = np.argsort(dist, kind="stable")[: 4 * a.top]
         cand = bits[order]
         ofn = crvec.ORACLE_NAME[name]
