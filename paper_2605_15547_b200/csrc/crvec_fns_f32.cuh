@@ -40,7 +40,7 @@ CR_F double with_sign(double a, uint32_t xb) {
 // ============================================================ exp family ====
 // exp_core: 2^(k/16) * e^r with |r| <= ln2/32 (fast path).
 CR_F double exp_core(int k, double r, double tab) {
-  double T = CR_TAB(tab, EXP2J_HI, k & 15);
+  double T = CR_TAB(tab, EXP2J_HI, k);  // shfl: source lane k mod 32 -> entry k & 15
   double p = fma_(mul_(r, r), expq(r), r);  // e^r - 1
   return scale2(fma_(T, p, T), k >> 4);
 }
@@ -49,7 +49,7 @@ CR_F double exp_core(int k, double r, double tab) {
 // result): the rounding-test tolerance E = 512 covers it with margin.
 CR_F double expq3(double r) { return fma_(fma_(fma_(EXPQ3[3], r, EXPQ3[2]), r, EXPQ3[1]), r, EXPQ3[0]); }
 CR_F double exp_core3(int k, double r, double tab) {
-  double T = CR_TAB(tab, EXP2J_HI, k & 15);
+  double T = CR_TAB(tab, EXP2J_HI, k);  // shfl: source lane k mod 32 -> entry k & 15
   double p = fma_(mul_(r, r), expq3(r), r);  // e^r - 1
   return scale2(fma_(T, p, T), k >> 4);
 }
@@ -185,9 +185,9 @@ struct FnExpm1 {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -18.5f), 89.5f)));
-    int j = q.k & 15, e = q.k >> 4;
-    double T = scale2(CR_TAB(R.t, EXP2J_HI, j), e);
-    double Tl = CR_TAB(R.tl, EXP2J_LO, j) * scale2(1.0, e);
+    int e = q.k >> 4;
+    double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
+    double Tl = CR_TAB(R.tl, EXP2J_LO, q.k) * scale2(1.0, e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     // main: 2^-26 < |x| < inf and x >= -18
     return Fast{fma_(T, p, add_(sub_(T, 1.0), Tl)),
@@ -226,8 +226,8 @@ struct HypParts {
 CR_F HypParts hyp_parts(double ax, double tab) {
   RedExp q = red_exp(ax);
   int kp = q.k, km = -q.k;
-  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp & 15), kp >> 4);
-  double Em = scale2(CR_TAB(tab, EXP2J_HI, km & 15), km >> 4);
+  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp), kp >> 4);
+  double Em = scale2(CR_TAB(tab, EXP2J_HI, km), km >> 4);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ[2], s, SINHQ[1]), s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(fma_(COSHQ[2], s, COSHQ[1]), s, COSHQ[0]), 1.0);
@@ -320,9 +320,9 @@ struct FnTanh {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(mul_(2.0, f2d(fminf(fabs_(x), 10.0f))));
-    int j = q.k & 15, e = q.k >> 4;
-    double T = scale2(CR_TAB(R.t, EXP2J_HI, j), e);
-    double Tl = CR_TAB(R.tl, EXP2J_LO, j) * scale2(1.0, e);
+    int e = q.k >> 4;
+    double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
+    double Tl = CR_TAB(R.tl, EXP2J_LO, q.k) * scale2(1.0, e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     double em1 = fma_(T, p, add_(sub_(T, 1.0), Tl));
     return Fast{with_sign(div_fast(em1, add_(em1, 2.0)), xb),
@@ -530,9 +530,12 @@ CR_F double sin_r(double r, double s) {
   return fma_(mul_(r, s), fma_(fma_(SINQ[2], s, SINQ[1]), s, SINQ[0]), r);
 }
 CR_F double cos_r(double s) { return fma_(s, fma_(fma_(COSQ[2], s, COSQ[1]), s, COSQ[0]), 1.0); }
+// sin(k pi/16) for any k: entry k mod 16 (shfl takes the source lane mod 32
+// and the table is replicated in both half-warps) with the sign of k & 16
+// flipped into the high word by one XOR.
 CR_F double sin16(double tab, int k) {
-  double v = CR_TAB(tab, SIN16_HI, k & 15);
-  return (k & 16) ? -v : v;
+  double v = CR_TAB(tab, SIN16_HI, k);
+  return hilo2d(d2hi(v) ^ ((k << 27) & (int)0x80000000), d2lo(v));
 }
 
 // DD sin/cos of r (|r| <= pi/32), Taylor to r^23.
@@ -646,8 +649,9 @@ using FnTan = FnTrig<2>;
 // tan(angle - theta_j) = (Y cos - X sin)/(X cos + Y sin), result theta_j +
 // atan(t); sin/cos of theta_j from one 16-entry table (cos theta_j = sin
 // theta_{15-j}).
-CR_F int atan_index(double Y, double X) {
-  float yf = (float)Y, xf = (float)X;
+// theta_j index from a cheap fp32 angle estimate (|error| < 0.004 rad, far
+// inside the half-spacing pi/60); inputs are binary32 copies of Y, X >= 0.
+CR_F int atan_index_f(float yf, float xf) {
   float mn = fminf(yf, xf), mx = fmaxf(yf, xf);
 #if CR_DEVICE
   float q = __fdividef(mn, mx);
@@ -660,13 +664,13 @@ CR_F int atan_index(double Y, double X) {
   int j = (int)rintf(ang * 9.5492966f);  // 30/pi
   return j < 0 ? 0 : (j > 15 ? 15 : j);
 }
+CR_F int atan_index(double Y, double X) { return atan_index_f((float)Y, (float)X); }
 CR_F double atan_t(double t) {
   double s = mul_(t, t);
   double q = fma_(fma_(fma_(ATANQ[3], s, ATANQ[2]), s, ATANQ[1]), s, ATANQ[0]);
   return fma_(mul_(t, s), q, t);
 }
-CR_F double atan2_core(double Y, double X, double tab) {
-  int j = atan_index(Y, X);
+CR_F double atan2_core(double Y, double X, double tab, int j) {
   double S = CR_TAB(tab, SIN30_HI, j), C = CR_TAB(tab, SIN30_HI, 15 - j);
   double num = fma_(Y, C, -mul_(X, S));
   double den = fma_(X, C, mul_(Y, S));
@@ -693,7 +697,8 @@ struct FnAtan {
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    return Fast{with_sign(atan2_core(f2d(fminf(fabs_(x), 0x1p127f)), 1.0, R.t), xb),
+    float ax = fminf(fabs_(x), 0x1p127f);
+    return Fast{with_sign(atan2_core(f2d(ax), 1.0, R.t, atan_index_f(ax, 1.0f)), xb),
                 in_range(xb << 1, 0x73000002u, 0xFF000002u)};  // 2^-12 < |x| <= inf
   }
   template <int M>
@@ -721,10 +726,11 @@ struct FnAsinAcos {
     double ax = f2d(fminf(fabs_(x), 1.0f));
     double s = sqrt_rn(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
     double a;
+    float axf = fminf(fabs_(x), 1.0f), sf = (float)s;
     if (!ACOS) {
-      a = with_sign(atan2_core(ax, s, R.t), xb);
+      a = with_sign(atan2_core(ax, s, R.t, atan_index_f(axf, sf)), xb);
     } else {
-      a = atan2_core(s, ax, R.t);
+      a = atan2_core(s, ax, R.t, atan_index_f(sf, axf));
       a = (int)xb < 0 ? add_(PI_H, -a) : a;
     }
     // asin main: 2^-12 < |x| <= 1; acos main: |x| <= 1 (acos(1) = 0 is

@@ -216,14 +216,19 @@ __global__ void __launch_bounds__(kThreads, KernelShape<F>::minb) k_map_vec(cons
   uint64_t base = warp * 32 * NV;
   float4 v[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = base + 32 * k + lane < n4 ? ld_stream(x + base + 32 * k + lane) : ones;
+  for (int k = 0; k < NV; ++k) {
+    uint64_t i = base + 32 * k + lane;
+    v[k] = ld_stream(x + (i < n4 ? i : n4 - 1));
+  }
   for (; base < n4; base += stride) {
     float4 nx[NV];
     float xs[4 * NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
+      // clamped address instead of a select: out-of-range lanes re-read the
+      // last float4 (discarded by the store predicate), no per-iteration MOVs
       uint64_t in = base + 32 * k + lane + stride;
-      nx[k] = in < n4 ? ld_stream(x + in) : ones;
+      nx[k] = ld_stream(x + (in < n4 ? in : n4 - 1));
       xs[4 * k] = v[k].x;
       xs[4 * k + 1] = v[k].y;
       xs[4 * k + 2] = v[k].z;
@@ -301,29 +306,45 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_sincos_vec(const float4 *x, float4 *ys, float4 *yc,
-                                                         uint64_t n4, unsigned long long *counters) {
+__global__ void __launch_bounds__(kThreads, 2) k_sincos_vec(const float4 *x, float4 *ys, float4 *yc,
+                                                            uint64_t n4, unsigned long long *counters) {
+  constexpr int NV = 2;
   PHBlock *sh = ph_storage<FnSin>();
   FnSin::Regs R;
   FnSin::load(R);
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  const uint64_t stride = nwarps * 32;
-  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
-  uint64_t base = warp * 32;
-  float4 v = base + lane < n4 ? ld_stream(x + base + lane) : ones;
+  const uint64_t stride = nwarps * 32 * NV;
+  uint64_t base = warp * 32 * NV;
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    uint64_t i = base + 32 * k + lane;
+    v[k] = ld_stream(x + (i < n4 ? i : n4 - 1));
+  }
   for (; base < n4; base += stride) {
-    uint64_t i = base + lane;
-    bool valid = i < n4;
-    float4 vn = i + stride < n4 ? ld_stream(x + i + stride) : ones;
-    float xs[4] = {v.x, v.y, v.z, v.w};
-    v = vn;
-    uint32_t s[4], c[4];
-    sincos_lanes<M, 4>(xs, s, c, R, sh, counters);
-    if (valid) {
-      st_stream(ys + i, make_float4(u2f(s[0]), u2f(s[1]), u2f(s[2]), u2f(s[3])));
-      st_stream(yc + i, make_float4(u2f(c[0]), u2f(c[1]), u2f(c[2]), u2f(c[3])));
+    float4 nx[NV];
+    float xs[4 * NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t in = base + 32 * k + lane + stride;
+      nx[k] = ld_stream(x + (in < n4 ? in : n4 - 1));
+      xs[4 * k] = v[k].x;
+      xs[4 * k + 1] = v[k].y;
+      xs[4 * k + 2] = v[k].z;
+      xs[4 * k + 3] = v[k].w;
+    }
+    uint32_t s[4 * NV], c[4 * NV];
+    sincos_lanes<M, 4 * NV>(xs, s, c, R, sh, counters);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      uint64_t i = base + 32 * k + lane;
+      if (i < n4) {
+        st_stream(ys + i, make_float4(u2f(s[4 * k]), u2f(s[4 * k + 1]), u2f(s[4 * k + 2]), u2f(s[4 * k + 3])));
+        st_stream(yc + i, make_float4(u2f(c[4 * k]), u2f(c[4 * k + 1]), u2f(c[4 * k + 2]), u2f(c[4 * k + 3])));
+      }
+      v[k] = nx[k];
     }
   }
 }
@@ -602,7 +623,7 @@ cudaError_t launch_sincos(const float *x, float *ys, float *yc, uint64_t n, cuda
   bool aligned = (((uintptr_t)x | (uintptr_t)ys | (uintptr_t)yc) & 15) == 0;
   uint64_t n4 = aligned ? n / 4 : 0;
   if (n4)
-    k_sincos_vec<M><<<grid_for((n4 + 31) / 32, mb_vec), kThreads, 0, s>>>(
+    k_sincos_vec<M><<<grid_for((n4 + 63) / 64, mb_vec), kThreads, 0, s>>>(
         (const float4 *)x, (float4 *)ys, (float4 *)yc, n4, ctr);
   uint64_t rem = n - 4 * n4;
   if (rem)

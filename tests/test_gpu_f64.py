@@ -119,3 +119,38 @@ def test_fast_path_stats(cuda):
         assert st.lanes == x.size
         assert st.undecided / x.size < 2.0 ** -15, (name, st)
         assert st.accurate_undecided == 0
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 33, 1001])
+def test_sizes_alignment_inplace_f64(cuda, oracle, n):
+    rng = np.random.default_rng(n)
+    x = rng.uniform(0.125, 8, n)
+    want = oracle.f64("log", x.view(np.uint64), 0) if n else np.zeros(0, np.uint64)
+    assert (crvec.cr_log(x, 0).view(np.uint64) == want).all()
+    buf = cuda.zeros(n + 1, dtype=cuda.float64, device="cuda")
+    buf[1:] = cuda.from_numpy(x).cuda()
+    v = buf[1:]                                   # 8-byte aligned only: scalar loads
+    L = crvec.lib()
+    s = cuda.cuda.current_stream()
+    import ctypes
+    assert L.crvec_log_dev(v.data_ptr(), v.data_ptr(), n, 0, ctypes.c_void_p(s.cuda_stream)) == 0  # in place
+    assert (v.cpu().numpy().view(np.uint64) == want).all()
+
+
+def test_concurrent_host_callers(cuda, oracle):
+    """Host-pointer calls from several threads share the staging workspace safely."""
+    import threading
+    rng = np.random.default_rng(9)
+    xs = [rng.uniform(0.1, 10, 300000).astype(np.float32) for _ in range(6)]
+    outs = [None] * 6
+
+    def work(i):
+        outs[i] = crvec.cr_logf(xs[i], i % 4)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(6):
+        assert (outs[i].view(np.uint32) == oracle.f32("log", xs[i].view(np.uint32), i % 4)).all()
