@@ -324,32 +324,38 @@ CR_F F64Out round_test64(double h, double l, double b) {
 constexpr double EPS_EXP2D = 0x1p-74;
 constexpr double EPS_LOGD = 0x1p-73;  // error analysis: < 2^-76
 
+// Lanes outside exp2's main range: NaN, +-Inf, overflow / underflow classes,
+// |x| <= 2^-55 (2^x in the gap beside 1) — all decided by rules.
+template <int M>
+CR_F double exp2d_special(double x) {
+  uint64_t xb = d2u(x);
+  if (x != x) return u2d(xb | 0x0008000000000000ull);
+  if (x == INFINITY) return INFINITY;
+  if (x >= 1024.0) return (M == RNE || M == RU) ? INFINITY : 0x1.fffffffffffffp1023;
+  if (x <= -1075.0) return (M == RU && x != -INFINITY) ? 0x1p-1074 : 0.0;  // tie at -1075 -> 0
+  if (x > 0) return M == RU ? 1.0 + 0x1p-52 : 1.0;                       // tiny
+  if (x < 0) return (M == RZ || M == RD) ? 1.0 - 0x1p-53 : 1.0;
+  return 1.0;                                                              // +-0
+}
+// main: 2^-55 < |x| < 1022 (bit-pattern range check); also (-1075, -1022]
+// (subnormal results) and [1022, 1024) go through the fast path + test.
+CR_F bool exp2d_main(double x) {
+  uint64_t a = d2u(x) & 0x7FFFFFFFFFFFFFFFull;
+  return a > 0x3C80000000000000ull && a < 0x4090CC0000000000ull;  // 2^-55 < |x| < 1075
+}
+
 template <int M>
 CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
-  uint64_t xb = d2u(x);
-  if (x != x) return {u2d(xb | 0x0008000000000000ull), true};
-  if (x == INFINITY) return {INFINITY, true};
-  if (x >= 1024.0) {
-    bool inf = M == RNE || M == RU;
-    return {inf ? INFINITY : 0x1.fffffffffffffp1023, true};
-  }
-  if (x <= -1075.0) {  // 2^x <= 2^-1075 (tie at -1075 rounds to even = 0)
-    return {M == RU && x != -INFINITY ? 0x1p-1074 : 0.0, true};
-  }
-  if (x == floor(x)) {  // exact power of two in [-1074, 1023]
-    int n = (int)x;
-    double p = n >= -1022 ? u2d((uint64_t)(n + 1023) << 52) : u2d(1ull << (n + 1074));
-    return {p, true};
-  }
-  if (dabs(x) <= 0x1p-55) {
-    if (x > 0) return {M == RU ? 1.0 + 0x1p-52 : 1.0, true};
-    return {(M == RZ || M == RD) ? 1.0 - 0x1p-53 : 1.0, true};
-  }
+  if (!exp2d_main(x) || x >= 1024.0) return {exp2d_special<M>(x), true};
   double t = fma_(x, 4096.0, SHIFTER);
   double kd = sub_(t, SHIFTER);
   int k = (int)d2lo(t);
   double R = fma_(kd, -0x1p-12, x);  // exact, |R| <= 2^-13
   int N = k >> 12, i1 = (k >> 8) & 15, i2 = (k >> 4) & 15, i3 = k & 15;
+  if (R == 0.0 && (k & 4095) == 0) {  // integer x: 2^x exact (normal or subnormal)
+    double p = N >= -1022 ? u2d((uint64_t)(N + 1023) << 52) : u2d(1ull << (N + 1074));
+    return {p, true};
+  }
   DD Tv = dd_mul(dd_mul(DD{T.t1h[i1], T.t1l[i1]}, DD{T.t2h[i2], T.t2l[i2]}), DD{T.t3h[i3], T.t3l[i3]});
   double q = fma_(fma_(fma_(fma_(EXP2D_Q[5], R, EXP2D_Q[4]), R, EXP2D_Q[3]), R, EXP2D_Q[2]), R,
                   EXP2D_Q[1]);
@@ -372,19 +378,7 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
 }
 
 template <int M>
-CR_F F64Out logd_fast(double x, const F64Tab &T) {
-  uint64_t xb = d2u(x);
-  if (x != x) return {u2d(xb | 0x0008000000000000ull), true};
-  if (x == 0.0) return {-INFINITY, true};
-  if (xb >> 63) return {u2d(0x7FF8000000000000ull), true};
-  if (x == INFINITY) return {INFINITY, true};
-  if (x == 1.0) return {0.0, true};
-  int eadj = 0;
-  double xs = x;
-  if (x < 0x1p-1022) {
-    xs = x * 0x1p54;
-    eadj = -54;
-  }
+CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   int h = d2hi(xs);
   int hh = h - 0x3FE80000;
   int e = (hh >> 20) + eadj;
@@ -411,6 +405,27 @@ CR_F F64Out logd_fast(double x, const F64Tab &T) {
   DD v = two_sum(th, b.hi);
   DD V = fast_two_sum(v.hi, add_(add_(v.lo, tl), small));
   return round_test64<M>(V.hi, V.lo, EPS_LOGD * dabs(V.hi));
+}
+
+
+// Lanes outside log's main range (positive normal, x != 1): NaN, +-0, x < 0,
+// +Inf, 1, and subnormals (scaled by 2^54 into the main computation).
+template <int M>
+CR_F F64Out logd_special(double x, const F64Tab &T) {
+  uint64_t xb = d2u(x);
+  if (x != x) return {u2d(xb | 0x0008000000000000ull), true};
+  if (x == 0.0) return {-INFINITY, true};
+  if (xb >> 63) return {u2d(0x7FF8000000000000ull), true};
+  if (x == INFINITY) return {INFINITY, true};
+  if (x == 1.0) return {0.0, true};
+  return logd_core<M>(x * 0x1p54, -54, T);  // subnormal
+}
+
+template <int M>
+CR_F F64Out logd_fast(double x, const F64Tab &T) {
+  uint64_t xb = d2u(x);
+  if (xb - 0x0010000000000000ull >= 0x7FE0000000000000ull || x == 1.0) return logd_special<M>(x, T);
+  return logd_core<M>(x, 0, T);
 }
 
 }  // namespace crvec

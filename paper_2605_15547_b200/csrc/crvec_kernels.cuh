@@ -148,11 +148,14 @@ __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      if (!f[e].main) {
-        ys[e] = F::template special<M>(xs[e]);
-      } else if (fail[e]) {
-        ys[e] = slow_round<F, M>(xs[e]);
-        ++cnt;
+      // warp-uniform skip of slots no lane needs (one vote per slot)
+      if (__any_sync(kFull, !f[e].main || fail[e])) {
+        if (!f[e].main) {
+          ys[e] = F::template special<M>(xs[e]);
+        } else if (fail[e]) {
+          ys[e] = slow_round<F, M>(xs[e]);
+          ++cnt;
+        }
       }
     }
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);

@@ -69,3 +69,53 @@ extern "C" int emu_eval(int fn, const uint32_t *x, uint32_t *y, uint64_t n, int 
   }
   return 0;
 }
+
+// Max |a - f(x)| of the fast path in units of ulp(a) (f from the accurate DD
+// path), over main lanes: the observed margin against the tolerance F::E.
+template <class F>
+static double probe(const uint32_t *x, uint64_t n, uint32_t *E) {
+  double worst = 0;
+  *E = F::E;
+  for (uint64_t i = 0; i < n; ++i) {
+    float xf = u2f(x[i]);
+    typename F::Regs R;
+    F::load(R);
+    Fast f;
+    if constexpr (is_trig<F>::value) {
+      RedTrig q = F::is_big(xf) ? ph_reduce(xf, INV_PI_WORDS) : red_trig_small(f2d(xf));
+      f = F::from_red(xf, q, R);
+    } else {
+      f = F::fast(xf, R);
+    }
+    if (!f.main || !std::isfinite(f.a) || f.a == 0) continue;
+    DD v = F::slow(xf);
+    double ulp = std::ldexp(1.0, std::ilogb(f.a) - 52);
+    double err = std::fabs((f.a - v.hi) - v.lo) / ulp;
+    if (err > worst) worst = err;
+  }
+  return worst;
+}
+
+extern "C" double emu_probe(int fn, const uint32_t *x, uint64_t n, uint32_t *E) {
+  switch (fn) {
+    case 0: return probe<FnExp2>(x, n, E);
+    case 1: return probe<FnLog>(x, n, E);
+    case 2: return probe<FnLog2>(x, n, E);
+    case 3: return probe<FnExp>(x, n, E);
+    case 4: return probe<FnExp10>(x, n, E);
+    case 5: return probe<FnExpm1>(x, n, E);
+    case 6: return probe<FnLog10>(x, n, E);
+    case 7: return probe<FnLog1p>(x, n, E);
+    case 8: return probe<FnSin>(x, n, E);
+    case 9: return probe<FnCos>(x, n, E);
+    case 10: return probe<FnTan>(x, n, E);
+    case 11: return probe<FnAsin>(x, n, E);
+    case 12: return probe<FnAcos>(x, n, E);
+    case 13: return probe<FnAtan>(x, n, E);
+    case 14: return probe<FnSinh>(x, n, E);
+    case 15: return probe<FnCosh>(x, n, E);
+    case 16: return probe<FnTanh>(x, n, E);
+    case 17: return probe<FnRsqrt>(x, n, E);
+  }
+  return -1;
+}
