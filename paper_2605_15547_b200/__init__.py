@@ -25,7 +25,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrvec.so")
+# CRVEC_LIB: developer override to load an A/B variant build (tools only).
+LIB_PATH = os.environ.get("CRVEC_LIB") or os.path.join(_HERE, "libcrvec.so")
 
 
 class CrvecError(RuntimeError):

@@ -34,44 +34,60 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _deps_newer(obj: str, src: str) -> bool:
+def _deps_newer(obj: str, src: str, csrc: str = CSRC) -> bool:
     if not os.path.exists(obj):
         return True
     t = os.path.getmtime(obj)
-    for f in os.listdir(CSRC):
-        if os.path.getmtime(os.path.join(CSRC, f)) > t:
+    for f in os.listdir(csrc):
+        if os.path.getmtime(os.path.join(csrc, f)) > t:
             return True
     return os.path.getmtime(os.path.join(ROOT, "include", "crvec.h")) > t
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+def build(force: bool = False, verbose: bool = False, csrc: str = CSRC, lib: str = LIB,
+          build_dir: str = BUILD) -> str:
+    """Compile the sources in `csrc` into `lib`. The defaults build the product
+    library; other directories are developer A/B variants (loaded through the
+    CRVEC_LIB environment variable by the perf tools)."""
+    CSRC_, LIB_, BUILD_ = csrc, lib, build_dir
+    os.makedirs(BUILD_, exist_ok=True)
+    srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC_, s))]
     objs = []
     jobs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         for s in srcs:
-            src = os.path.join(CSRC, s)
-            obj = os.path.join(BUILD, s.replace(".cu", ".o"))
+            src = os.path.join(CSRC_, s)
+            obj = os.path.join(BUILD_, s.replace(".cu", ".o"))
             objs.append(obj)
-            if force or _deps_newer(obj, src):
+            if force or _deps_newer(obj, src, CSRC_):
                 cmd = [nvcc(), *ARCH, *FLAGS, "-Xptxas", "-v", "-c", src, "-o", obj]
                 jobs.append((s, ex.submit(subprocess.run, cmd, capture_output=True, text=True)))
         for s, fut in jobs:
             r = fut.result()
-            with open(os.path.join(BUILD, s + ".log"), "w") as f:
+            with open(os.path.join(BUILD_, s + ".log"), "w") as f:
                 f.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed on {s}:\n{r.stderr[-4000:]}")
-    if force or jobs or not os.path.exists(LIB):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    if force or jobs or not os.path.exists(LIB_):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB_, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr[-4000:])
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", LIB_)
+    return LIB_
+
+
+def build_variant(name: str, csrc: str) -> str:
+    """Developer A/B build: sources from `csrc` -> variants/libcrvec_<name>.so."""
+    vdir = os.path.join(PKG, "variants")
+    return build(verbose=True, csrc=csrc, lib=os.path.join(vdir, f"libcrvec_{name}.so"),
+                 build_dir=os.path.join(vdir, "_build_" + name))
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        build_variant(sys.argv[i + 1], sys.argv[i + 2])
+    else:
+        build(force="--force" in sys.argv, verbose=True)

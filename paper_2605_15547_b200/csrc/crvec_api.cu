@@ -10,7 +10,7 @@
 #include <cstring>
 #include <mutex>
 
-#include "../../include/crvec.h"
+#include "crvec.h"
 #include "crvec_kernels.cuh"
 
 namespace crvec {

@@ -60,7 +60,12 @@ CR_F double rcp_approx(double x) {
 }
 CR_F double rsqrt_approx(double x) {
   double r;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x));
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));  // one MUFU.RSQ64H (the non-ftz form adds a range fix-up call)
+  return r;
+}
+CR_F float rcp_approx_f(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // one MUFU.RCP
   return r;
 }
 CR_F double sqrt_rn(double x) { return __dsqrt_rn(x); }
@@ -90,6 +95,7 @@ CR_F double dabs(double a) { return std::fabs(a); }
 CR_F float fabs_(float a) { return std::fabs(a); }
 CR_F double rcp_approx(double x) { return (double)(float)(1.0 / x); }
 CR_F double rsqrt_approx(double x) { return (double)(float)(1.0 / std::sqrt(x)); }
+CR_F float rcp_approx_f(float x) { return 1.0f / x; }
 CR_F double sqrt_rn(double x) { return std::sqrt(x); }
 CR_F int clz32(uint32_t v) { return v ? __builtin_clz(v) : 32; }
 template <int M>
@@ -186,15 +192,17 @@ CR_F DD dd_horner(const double *chi, const double *clo, int n, DD x) {
 // ------------------------------------------------ rounding decisions ----
 // Fast-path rounding test. `a` approximates f(x) with relative error below
 // E * 2^-53. The binary32 rounding boundaries for every mode (representable
-// values and midpoints) are the doubles whose low 28 significand bits are
-// zero (53 - 25 = 28); subnormal binary32 boundaries are a subset. The lane
-// is decided iff a is more than E double-ulps away from every boundary — the
-// Ziv straddle test of ref: proj/src/kernels_f64.cpp:63-76 on the 32-bit low
-// word (3 integer ops).
-CR_F bool near_boundary(double a, uint32_t E) {
-  uint32_t t = (d2lo(a) + E) & 0x0FFFFFFFu;
-  return t <= 2u * E;
+// values and midpoints, subnormals included) are the doubles whose low 28
+// significand bits are zero (53 - 25 = 28); subnormal binary32 boundaries are
+// a subset. The lane is decided iff a is outside the window [-2E, 2E) double
+// ulps around every such double (which contains the +-E of the error bound):
+// the Ziv straddle test of ref: proj/src/kernels_f64.cpp:63-76 on the 32-bit
+// low word. E is a power of two, so the window test is one add and one
+// LOP3 with a predicate output: ((lo + 2E) mod 2^28) < 4E.
+CR_F bool near_boundary_lo(uint32_t lo, uint32_t E) {
+  return ((lo + 2u * E) & (0x0FFFFFFFu & ~(4u * E - 1u))) == 0u;
 }
+CR_F bool near_boundary(double a, uint32_t E) { return near_boundary_lo(d2lo(a), E); }
 
 // Correct rounding of a double-double h + l (|h + l - f| <= 2^-90 |f|):
 // snap to an exactly representable binary32 when within 2^-80 (binary32
@@ -238,14 +246,17 @@ CR_F bool nan_bits(uint32_t xb) { return (xb << 1) > 0xFF000000u; }
 // quiet(x): payload and sign kept (ref: proj/include/crvec/fpbits.hpp:101-102).
 CR_F uint32_t quiet_bits(uint32_t xb) { return xb | 0x00400000u; }
 
-// sqrt(a) for a in [0, 1] to ~2^-52 relative: MUFU seed, one rsqrt Newton
-// step, one Karp-Markstein correction (7 FP64 ops; a = 0 -> 0).
+// sqrt(a) for a normal, positive a to ~2^-52 relative (a = 0 gives NaN: the
+// callers keep such lanes off the main path): MUFU.RSQ64H seed y0, one
+// coupled Newton step on (s, h) = (a*y0, y0/2), one Karp-Markstein
+// correction. 1 MUFU + 2 DMUL + 5 DFMA.
 CR_F double sqrt_fast(double a) {
   double y = rsqrt_approx(a);
-  y = fma_(mul_(y, 0.5), fma_(-mul_(a, y), y, 1.0), y);
-  double s = mul_(a, y);
-  s = fma_(fma_(-s, s, a), mul_(y, 0.5), s);
-  return a > 0.0 ? s : 0.0;
+  double s = mul_(a, y), h = mul_(y, 0.5);
+  double r = fma_(-s, h, 0.5);
+  s = fma_(s, r, s);
+  h = fma_(h, r, h);
+  return fma_(fma_(-s, s, a), h, s);
 }
 
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);

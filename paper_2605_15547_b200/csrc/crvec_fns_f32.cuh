@@ -106,8 +106,9 @@ struct FnExp {
   CR_F static Fast fast(float x, const Regs &R) {
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -104.5f), 89.5f)));
     // main: 2^-26 < |x| < inf (saturation is handled by the clamp)
-    return Fast{exp_core3(q.k, q.r, R.t), in_range(f2u(x) << 1, 0x65000002u, 0xFF000000u)};
+    return Fast{exp_core3(q.k, q.r, R.t), in_main(f2u(x))};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x65000002u, 0xFF000000u); }
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -129,9 +130,9 @@ struct FnExp2 {
     double u = fma_(kd, -0.0625, xc);  // exact
     // integer x gives 2^x exactly: the rounding test sends it to the accurate
     // path, whose exact-value snap returns it in every mode.
-    return Fast{exp_core3((int)d2lo(t), mul_(u, LN2_D), R.t),
-                in_range(f2u(x) << 1, 0x65000002u, 0xFF000000u)};
+    return Fast{exp_core3((int)d2lo(t), mul_(u, LN2_D), R.t), in_main(f2u(x))};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x65000002u, 0xFF000000u); }
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -157,8 +158,9 @@ struct FnExp10 {
     r = fma_(xc, LN10_M, r);
     r = fma_(kd, -LN2_16_M, r);
     r = fma_(xc, LN10_L, r);
-    return Fast{exp_core3((int)d2lo(t), r, R.t), in_range(f2u(x) << 1, 0x63000002u, 0xFF000000u)};
+    return Fast{exp_core3((int)d2lo(t), r, R.t), in_main(f2u(x))};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x63000002u, 0xFF000000u); }
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -186,9 +188,12 @@ struct FnExpm1 {
     double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     // main: 2^-26 < |x| < inf and x >= -18
-    return Fast{fma_(T, p, sub_(T, 1.0)),
-                in_range(xb << 1, 0x65000002u, 0xFF000000u) && xb <= 0xC1900000u};
+    return Fast{fma_(T, p, sub_(T, 1.0)), in_main(xb)};
   }
+  // main: 2^-26 < |x| < inf. x < -18.5 takes the clamp: expm1(-18.5) lies in
+  // (-1, -1 + 2^-26), which holds no binary32 rounding boundary, so it rounds
+  // like the true value in every mode.
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x65000002u, 0xFF000000u); }
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -262,9 +267,9 @@ struct FnSinh {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
-    return Fast{with_sign(fma_(h.Sa, h.cr, mul_(h.Ca, h.sr)), xb),
-                in_range(xb << 1, 0x73000002u, 0xFF000000u)};  // 2^-12 < |x| < inf
+    return Fast{with_sign(fma_(h.Sa, h.cr, mul_(h.Ca, h.sr)), xb), in_main(xb)};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000000u); }  // 2^-12 < |x| < inf
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -287,9 +292,9 @@ struct FnCosh {
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
-    return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)),
-                in_range(f2u(x) << 1, 0x72000002u, 0xFF000000u)};  // 2^-13 < |x| < inf
+    return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)), in_main(f2u(x))};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x72000002u, 0xFF000000u); }  // 2^-13 < |x| < inf
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -317,9 +322,12 @@ struct FnTanh {
     double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     double em1 = fma_(T, p, sub_(T, 1.0));
-    return Fast{with_sign(div_fast(em1, add_(em1, 2.0)), xb),
-                in_range(xb << 1, 0x73000002u, 0x82400000u)};  // 2^-12 < |x| < 10
+    return Fast{with_sign(div_fast(em1, add_(em1, 2.0)), xb), in_main(xb)};
   }
+  // main: 2^-12 < |x| < inf. |x| > 10 takes the clamp: tanh(10) lies in
+  // (1 - 2^-27, 1), which holds no binary32 rounding boundary, so it rounds
+  // like the true value in every mode.
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000000u); }
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -348,11 +356,14 @@ struct RedLog {
   int e, i;
   double m;
 };
+// `i` is the raw bin index: the register-table shuffle reads lane i mod 32,
+// which holds entry i mod 16 (the table is replicated in both half-warps), so
+// the fast path needs no mask; direct table reads use i & 15.
 CR_F RedLog red_log(double xd) {
   int h = d2hi(xd);
   int hh = h - 0x3FE88000;
   int e = hh >> 20;
-  return {e, (hh >> 16) & 15, hilo2d(h - (e << 20), d2lo(xd))};
+  return {e, hh >> 16, hilo2d(h - (int)((uint32_t)e << 20), d2lo(xd))};
 }
 
 template <int BASE>  // 0: ln, 2: log2, 10: log10
@@ -377,8 +388,9 @@ struct FnLogB {
     else a = fma_(p, INV_LN10, fma_(ed, LOG10_2, L));
     // main: 0 < x < +Inf. Exact results (x = 1, 2^k, 10^k) fail the rounding
     // test and are returned exactly by the accurate path's snap.
-    return Fast{a, xb - 1u < 0x7F7FFFFFu};
+    return Fast{a, in_main(xb)};
   }
+  CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < +Inf
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
@@ -400,8 +412,8 @@ struct FnLogB {
   }
   CR_F static DD slow(float x) {
     RedLog q = red_log(f2d(x));
-    double r = fma_(q.m, (double)LOG_C[q.i], -1.0);  // exact
-    return log_dd_core(q.e, q.i, DD{r, 0.0});
+    double r = fma_(q.m, (double)LOG_C[q.i & 15], -1.0);  // exact
+    return log_dd_core(q.e, q.i & 15, DD{r, 0.0});
   }
 };
 using FnLog = FnLogB<0>;
@@ -429,8 +441,9 @@ struct FnLog1p {
     double xd = f2d(x);
     if ((xb << 1) <= 0x65000000u) a = fma_(-dabs(xd), 0x1p-36, xd);
     // main: 0 < |x| < inf and x > -1
-    return Fast{a, in_range(xb << 1, 2u, 0xFF000000u) && xb < 0xBF800000u};
+    return Fast{a, in_main(xb)};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 2u, 0xFF000000u) && xb < 0xBF800000u; }
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -449,9 +462,9 @@ struct FnLog1p {
     if ((f2u(x) << 1) <= 0x65000000u) return DD{xd, -dabs(xd) * 0x1p-36};
     DD y = two_sum(1.0, xd);  // 1 + x = y.hi + y.lo exactly
     RedLog q = red_log(y.hi);
-    DD pm = two_prod(q.m, (double)LOG_C[q.i]);
+    DD pm = two_prod(q.m, (double)LOG_C[q.i & 15]);
     DD r = fast_two_sum(sub_(pm.hi, 1.0), pm.lo);
-    DD v = FnLogB<0>::log_dd_core(q.e, q.i, r);
+    DD v = FnLogB<0>::log_dd_core(q.e, q.i & 15, r);
     // log(1 + x) = log(y.hi) + log1p(u), u = y.lo / y.hi (|u| <= 2^-53, or
     // u = x itself when x is tiny and y.hi == 1): u - u^2/2 + u^3/3 - u^4/4.
     double u = y.lo / y.hi;
@@ -601,7 +614,10 @@ struct FnTrig {
     else if (WHICH == 1) a = fma_(Ck, cr, -mul_(Sk, sr));
     else a = div_fast(fma_(Sk, cr, mul_(Ck, sr)), fma_(Ck, cr, -mul_(Sk, sr)));
     // main: tiny threshold < |x| < inf (sin 2^-12, cos/tan 2^-13)
-    return Fast{a, in_range(f2u(x) << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u)};
+    return Fast{a, in_main(f2u(x))};
+  }
+  CR_F static bool in_main(uint32_t xb) {
+    return in_range(xb << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u);
   }
   CR_F static bool is_big(float x) {
     uint32_t az = f2u(x) << 1;
@@ -683,16 +699,36 @@ CR_F DD atan2_core_dd(DD Y, DD X) {
   return dd_add(th, p);
 }
 
+// atan by angle subtraction (tools/gen_tables.py gen_atan): with z = |x| and
+// a table angle A_k near atan z, atan z = A_k + atan((z C_k - S_k)/(C_k + z S_k)),
+// |t| <= 0.069. Entry k = j + 8*up, up = (z > 1), j = RN(7.49 * min(z, 1/z)):
+// the index needs one fp32 reciprocal, no angle estimate.
+CR_F double atan_t2(double t) {
+  double s = mul_(t, t);
+  double q = fma_(fma_(fma_(ATANQ2[3], s, ATANQ2[2]), s, ATANQ2[1]), s, ATANQ2[0]);
+  return fma_(mul_(t, s), q, t);
+}
+
 struct FnAtan {
-  static constexpr uint32_t E = 32;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
+  static constexpr uint32_t E = 64;
+  struct Regs { int a; double c, s; };
+  CR_F static void load(Regs &R) {
+    R.a = CR_TAB_LOAD(ATAN_A_HI);
+    R.c = CR_TAB_LOAD(ATAN_C);
+    R.s = CR_TAB_LOAD(ATAN_S);
+  }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    float ax = fminf(fabs_(x), 0x1p127f);
-    return Fast{with_sign(atan2_core(f2d(ax), 1.0, R.t, atan_index_f(ax, 1.0f)), xb),
-                in_range(xb << 1, 0x73000002u, 0xFF000002u)};  // 2^-12 < |x| <= inf
+    float axf = fminf(fabs_(x), 0x1p127f);
+    double z = f2d(axf);
+    bool up = axf > 1.0f;
+    int k = (int)f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f)) + (up ? 8 : 0);
+    double A = hilo2d(CR_TAB(R.a, ATAN_A_HI, k), 0u);
+    double C = CR_TAB(R.c, ATAN_C, k), S = CR_TAB(R.s, ATAN_S, k);
+    double t = div_fast(fma_(z, C, -S), fma_(z, S, C));
+    return Fast{with_sign(add_(A, atan_t2(t)), xb), in_main(xb)};
   }
+  CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000002u); }  // 2^-12 < |x| <= inf
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
@@ -708,32 +744,61 @@ struct FnAtan {
   }
 };
 
+// asin / acos without a division: with theta = asin|x| (or acos|x|), s =
+// sqrt(1 - x^2) and a table angle A_k near theta,
+//   sin(theta - A_k) = |x| cos A_k - s sin A_k        (asin)
+//   sin(phi - B_k)   = s cos B_k - |x| sin B_k        (acos, phi = acos|x|)
+// so the result is A_k + asin(d) with |d| <= 0.064 and a degree-3 odd
+// polynomial in d^2. Entry k = j + 8*up: up = (|x| > s) selects the upper
+// half-angle range and j = RN(10.5 * min(|x|, s)) (tools/gen_tables.py
+// gen_asin). The angles have 21 significant bits: one shuffled word each.
+CR_F double asinq(double d) {
+  double z = mul_(d, d);
+  double q = fma_(fma_(fma_(ASINQ[3], z, ASINQ[2]), z, ASINQ[1]), z, ASINQ[0]);
+  return fma_(mul_(d, z), q, d);
+}
+
 template <bool ACOS>
 struct FnAsinAcos {
   static constexpr uint32_t E = 64;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN30_HI); }
+  struct Regs { int a; double c, s; };
+  CR_F static void load(Regs &R) {
+    R.a = ACOS ? CR_TAB_LOAD(ACOS_A_HI) : CR_TAB_LOAD(ASIN_A_HI);
+    R.c = ACOS ? CR_TAB_LOAD(ACOS_C) : CR_TAB_LOAD(ASIN_C);
+    R.s = ACOS ? CR_TAB_LOAD(ACOS_S) : CR_TAB_LOAD(ASIN_S);
+  }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    double ax = f2d(fminf(fabs_(x), 1.0f));
-    double s = sqrt_rn(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
-    double a;
-    float axf = fminf(fabs_(x), 1.0f), sf = (float)s;
-    if (!ACOS) {
-      a = with_sign(atan2_core(ax, s, R.t, atan_index_f(axf, sf)), xb);
-    } else {
-      a = atan2_core(s, ax, R.t, atan_index_f(sf, axf));
-      a = (int)xb < 0 ? add_(PI_H, -a) : a;
-    }
-    // asin main: 2^-12 < |x| <= 1; acos main: |x| <= 1 (acos(1) = 0 is
-    // snapped exactly by the accurate path)
-    return Fast{a, ACOS ? (xb << 1) <= 0x7F000000u : in_range(xb << 1, 0x73000002u, 0x7F000002u)};
+    float axf = fminf(fabs_(x), 1.0f);
+    double ax = f2d(axf);
+    double s = sqrt_fast(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
+    float sf = (float)s;
+    bool up = axf > sf;
+    // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; the
+    // shuffle reads lane k mod 32 (table replicated in both half-warps)
+    int k = (int)f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f)) + (up ? 8 : 0);
+    double A = hilo2d(ACOS ? CR_TAB(R.a, ACOS_A_HI, k) : CR_TAB(R.a, ASIN_A_HI, k), 0u);
+    double C = ACOS ? CR_TAB(R.c, ACOS_C, k) : CR_TAB(R.c, ASIN_C, k);
+    double S = ACOS ? CR_TAB(R.s, ACOS_S, k) : CR_TAB(R.s, ASIN_S, k);
+    double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
+    double a = add_(A, asinq(d));
+    if (!ACOS) a = with_sign(a, xb);
+    else a = (int)xb < 0 ? add_(PI_H, -a) : a;
+    return Fast{a, in_main(xb)};
+  }
+  // asin main: 2^-12 < |x| < 1; acos main: |x| < 1 (s > 0 on the main path)
+  CR_F static bool in_main(uint32_t xb) {
+    return ACOS ? (xb << 1) < 0x7F000000u : in_range(xb << 1, 0x73000002u, 0x7F000000u);
   }
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
     if (nan_bits(xb)) return quiet_bits(xb);
     if ((xb << 1) > 0x7F000000u) return 0x7FC00000u;  // |x| > 1
+    if ((xb << 1) == 0x7F000000u) {                   // |x| = 1: +-pi/2, 0, pi
+      if (!ACOS) return f2u(cvt_f32<M>(with_sign(0.5 * PI_H, xb)));
+      return (int)xb < 0 ? f2u(cvt_f32<M>(PI_H)) : 0u;
+    }
     if ((xb << 1) == 0) return xb;                    // asin(+-0)
     double xd = f2d(x);
     return f2u(cvt_f32<M>(fma_(xd, 0x1p-36, xd)));   // asin: x + x^3/6 just above |x|
@@ -767,8 +832,9 @@ struct FnRsqrt {
     return y;
   }
   CR_F static Fast fast(float x, const Regs &) {
-    return Fast{newton(f2d(x)), f2u(x) - 1u < 0x7F7FFFFFu};  // 0 < x < inf
+    return Fast{newton(f2d(x)), in_main(f2u(x))};
   }
+  CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < inf
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);

@@ -129,37 +129,69 @@ __device__ __forceinline__ void fast_lanes(const float (&xs)[NE], Fast (&f)[NE],
   }
 }
 
+// Common path for NE elements per lane: fast approximation, one static-mode
+// conversion, and the per-lane mask of rare slots (bit e: slot e is outside
+// the main range, or undecided by the rounding test).
+template <class F, int M, int NE>
+__device__ __forceinline__ unsigned fast_eval(const float (&xs)[NE], uint32_t (&ys)[NE],
+                                              const typename F::Regs &R, PHBlock *sh) {
+  static_assert((F::E & (F::E - 1)) == 0 && F::E <= (1u << 24), "E: power of two");
+  Fast f[NE];
+  fast_lanes<F, NE>(xs, f, R, sh);
+  unsigned mask = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    ys[e] = f2u(cvt_f32<M>(f[e].a));
+    mask |= (unsigned)((!f[e].main) | near_boundary(f[e].a, F::E)) << e;
+  }
+  return mask;
+}
+
+// One rare lane value: IEEE special / tiny / saturation rule, or the
+// double-double accurate path (counted).
+template <class F, int M>
+__device__ __forceinline__ uint32_t resolve_one(float x, int &cnt) {
+  if (F::in_main(f2u(x))) {
+    ++cnt;
+    return slow_round<F, M>(x);
+  }
+  return F::template special<M>(x);
+}
+
+template <int NE>
+__device__ __forceinline__ float gather_slot(const float (&xs)[NE], unsigned low) {
+  float xe = xs[0];
+#pragma unroll
+  for (int e = 1; e < NE; ++e) xe = (low >> e) & 1u ? xs[e] : xe;
+  return xe;
+}
+
+// Rare path (register form, scalar kernels): each pass takes every lane's
+// lowest pending slot, gathers its input with selects (no dynamic register
+// indexing), resolves it and scatters the result back; a lane rarely has two
+// pending slots, so one pass usually serves the whole warp.
+template <class F, int M, int NE>
+__device__ __forceinline__ void resolve_rare(const float (&xs)[NE], uint32_t (&ys)[NE], unsigned mask,
+                                             unsigned long long *counters) {
+  int cnt = 0;
+  do {
+    const unsigned low = mask & (0u - mask);
+    const float xe = gather_slot<NE>(xs, low);
+    uint32_t r = 0;
+    if (low) r = resolve_one<F, M>(xe, cnt);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) ys[e] = (low >> e) & 1u ? r : ys[e];
+    mask &= ~low;
+  } while (__any_sync(kFull, mask != 0));
+  if (cnt) atomicAdd(counters, (unsigned long long)cnt);
+}
+
 template <class F, int M, int NE>
 __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)[NE],
                                            const typename F::Regs &R, PHBlock *sh,
                                            unsigned long long *counters) {
-  Fast f[NE];
-  fast_lanes<F, NE>(xs, f, R, sh);
-  bool fail[NE];
-  bool rare = false;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    ys[e] = finish<M>(f[e], fail[e], F::E);
-    rare |= fail[e] | !f[e].main;
-  }
-  // Rare, warp-uniform branch: specials / tiny / saturated lanes and lanes the
-  // rounding test could not decide (accurate path, ~2^-24 of random inputs).
-  if (__any_sync(kFull, rare)) {
-    int cnt = 0;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      // warp-uniform skip of slots no lane needs (one vote per slot)
-      if (__any_sync(kFull, !f[e].main || fail[e])) {
-        if (!f[e].main) {
-          ys[e] = F::template special<M>(xs[e]);
-        } else if (fail[e]) {
-          ys[e] = slow_round<F, M>(xs[e]);
-          ++cnt;
-        }
-      }
-    }
-    if (cnt) atomicAdd(counters, (unsigned long long)cnt);
-  }
+  const unsigned mask = fast_eval<F, M, NE>(xs, ys, R, sh);
+  if (__any_sync(kFull, mask != 0)) resolve_rare<F, M, NE>(xs, ys, mask, counters);
 }
 
 // Shared staging exists only in the trig kernels (34 KB per block).
@@ -178,74 +210,84 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // ------------------------------------------------------------ map kernels ----
 // 4 elements (one float4) per lane per iteration; the loop trip count is
 // warp-uniform so the register-table shuffles always see a full warp.
-// Kernel shape per function, chosen by measurement (tools/membench.cu,
-// profiles/r01/membench2.txt): float4s per lane per iteration (NV) and the
-// __launch_bounds__ min-blocks register cap (MINB).
+// Kernel shape per function, chosen by measurement (tools/gpu_shapes.sh over
+// tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw1.txt): float4s
+// per lane per step (nv) and the __launch_bounds__ min-blocks register cap
+// (minb; 256 threads per block).
 template <class F>
 struct KernelShape {
   static constexpr int nv = 2, minb = 3;
 };
-template <>
-struct KernelShape<FnLog1p> {
-  static constexpr int nv = 2, minb = 1;
-};
-template <int W>
-struct KernelShape<FnTrig<W>> {
-  static constexpr int nv = 2, minb = 2;
-};
-template <bool A>
-struct KernelShape<FnAsinAcos<A>> {
-  static constexpr int nv = 1, minb = 4;
-};
+template <> struct KernelShape<FnExp2> { static constexpr int nv = 4, minb = 2; };
+template <> struct KernelShape<FnExp10> { static constexpr int nv = 4, minb = 2; };
+template <> struct KernelShape<FnExp> { static constexpr int nv = 2, minb = 4; };
+template <> struct KernelShape<FnExpm1> { static constexpr int nv = 1, minb = 5; };
+template <> struct KernelShape<FnTanh> { static constexpr int nv = 1, minb = 4; };
+template <> struct KernelShape<FnLog1p> { static constexpr int nv = 2, minb = 4; };
+template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int nv = 1, minb = 4; };
 template <class F>
 struct VecWidth {
   static constexpr int value = KernelShape<F>::nv;
 };
 
+// One grid-stride step of the map kernel: issue the loads of the next step
+// into `nxt`, evaluate `cur`, store. Called alternately with the two register
+// buffers swapped, so the double buffer needs no register moves.
+template <class F, int M, int NV>
+__device__ __forceinline__ void map_step(const float4 *__restrict__ x, float4 *__restrict__ y,
+                                         uint32_t n4, uint32_t base, uint32_t stride,
+                                         const float4 (&cur)[NV], float4 (&nxt)[NV],
+                                         const typename F::Regs &R, PHBlock *sh,
+                                         unsigned long long *counters) {
+  float xs[4 * NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t in = base + stride + 32 * k;
+    if (in < n4) nxt[k] = ld_stream(x + in);
+    xs[4 * k] = cur[k].x;
+    xs[4 * k + 1] = cur[k].y;
+    xs[4 * k + 2] = cur[k].z;
+    xs[4 * k + 3] = cur[k].w;
+  }
+  uint32_t ys[4 * NV];
+  eval_lanes<F, M, 4 * NV>(xs, ys, R, sh, counters);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t i = base + 32 * k;
+    if (i < n4)
+      st_stream(y + i, make_float4(u2f(ys[4 * k]), u2f(ys[4 * k + 1]), u2f(ys[4 * k + 2]),
+                                   u2f(ys[4 * k + 3])));
+  }
+}
+
 template <class F, int M>
-__global__ void __launch_bounds__(kThreads, KernelShape<F>::minb) k_map_vec(const float4 *x, float4 *y, uint64_t n4,
-                                                      unsigned long long *counters) {
+__global__ void __launch_bounds__(kThreads, KernelShape<F>::minb)
+    k_map_vec(const float4 *__restrict__ x, float4 *__restrict__ y, uint32_t n4,
+              unsigned long long *counters) {
   constexpr int NV = VecWidth<F>::value;
   PHBlock *sh = ph_storage<F>();
   typename F::Regs R;
   F::load(R);
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  // Each warp handles NV x 32 float4 per iteration and requests the next
-  // iteration's float4s before computing this one (register double buffer).
-  const uint64_t stride = nwarps * 32 * NV;
-  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
-  uint64_t base = warp * 32 * NV;
-  float4 v[NV];
+  // 32-bit float4 indices (the launcher keeps n4 <= 2^31): one IMAD.WIDE per
+  // address, one compare per access. Each warp handles NV x 32 float4 per
+  // step; the trip count is warp-uniform (register-table shuffles need the
+  // whole warp).
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * (uint32_t)(kThreads * NV);
+  uint32_t base = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 * NV) + lane;
+  float4 va[NV], vb[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    uint64_t i = base + 32 * k + lane;
-    v[k] = ld_stream(x + (i < n4 ? i : n4 - 1));
+    va[k] = make_float4(1.f, 1.f, 1.f, 1.f);
+    vb[k] = va[k];
+    if (base + 32 * k < n4) va[k] = ld_stream(x + base + 32 * k);
   }
-  for (; base < n4; base += stride) {
-    float4 nx[NV];
-    float xs[4 * NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      // clamped address instead of a select: out-of-range lanes re-read the
-      // last float4 (discarded by the store predicate), no per-iteration MOVs
-      uint64_t in = base + 32 * k + lane + stride;
-      nx[k] = ld_stream(x + (in < n4 ? in : n4 - 1));
-      xs[4 * k] = v[k].x;
-      xs[4 * k + 1] = v[k].y;
-      xs[4 * k + 2] = v[k].z;
-      xs[4 * k + 3] = v[k].w;
-    }
-    uint32_t ys[4 * NV];
-    eval_lanes<F, M, 4 * NV>(xs, ys, R, sh, counters);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      uint64_t i = base + 32 * k + lane;
-      if (i < n4)
-        st_stream(y + i, make_float4(u2f(ys[4 * k]), u2f(ys[4 * k + 1]), u2f(ys[4 * k + 2]), u2f(ys[4 * k + 3])));
-      v[k] = nx[k];
-    }
+  while (base - lane < n4) {
+    map_step<F, M, NV>(x, y, n4, base, stride, va, vb, R, sh, counters);
+    base += stride;
+    if (base - lane >= n4) break;
+    map_step<F, M, NV>(x, y, n4, base, stride, vb, va, R, sh, counters);
+    base += stride;
   }
 }
 
@@ -606,9 +648,12 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
   static int mb_sc = max_blocks(k_map_scalar<F, M>);
   bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
   uint64_t n4 = aligned ? n / 4 : 0;
-  if (n4) {
-    k_map_vec<F, M><<<grid_for((n4 + 32 * VecWidth<F>::value - 1) / (32 * VecWidth<F>::value), mb_vec), kThreads, 0, s>>>(
-        (const float4 *)x, (float4 *)y, n4, ctr);
+  // the kernel indexes float4s with 32 bits: launches of at most 2^31 float4s
+  constexpr uint64_t kMaxN4 = uint64_t(1) << 31;
+  for (uint64_t off = 0; off < n4; off += kMaxN4) {
+    uint64_t m = n4 - off < kMaxN4 ? n4 - off : kMaxN4;
+    k_map_vec<F, M><<<grid_for((m + 32 * VecWidth<F>::value - 1) / (32 * VecWidth<F>::value), mb_vec),
+                      kThreads, 0, s>>>((const float4 *)x + off, (float4 *)y + off, (uint32_t)m, ctr);
   }
   uint64_t rem = n - 4 * n4;
   if (rem) {

@@ -62,3 +62,44 @@ def trig_input(n: int, seed: int = 4) -> np.ndarray:
     s = rng.integers(0, 2, n, dtype=np.uint64).astype(np.uint32) << np.uint32(31)
     big = s | (e << np.uint32(23)) | m
     return np.where(rng.integers(0, 8, n) == 0, big, x)
+
+
+def device_input(name: str, n: int, dist: str = "config", seed: int = 7, device: str = "cuda"):
+    """The same distributions as above generated on the device with torch (for
+    the perf tools: 2^28-element inputs in milliseconds; not bit-identical to
+    the numpy generators). Returns a float32 tensor."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def ubits(m, hi=2**32):
+        return torch.randint(0, hi, (m,), generator=g, device=device, dtype=torch.int64)
+
+    lo, hi = RANGES[name]
+    if dist == "uniform" or name not in ("logf", "log2f", "log10f", "log1pf", "sinf", "cosf",
+                                         "tanf", "sincosf"):
+        u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        return (lo + (hi - lo) * u).to(torch.float32)
+    if name in ("sinf", "cosf", "tanf", "sincosf"):
+        u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        x = (-100 + 200 * u).to(torch.float32).view(torch.int32).to(torch.int64)
+        e = torch.randint(142, 255, (n,), generator=g, device=device)
+        m = ubits(n, 1 << 23)
+        s = ubits(n, 2) << 31
+        big = s | (e << 23) | m
+        x = torch.where(torch.randint(0, 8, (n,), generator=g, device=device) == 0, big, x)
+    else:
+        x = ubits(n, 0x7F800000)
+        k = torch.randint(0, 1000, (n,), generator=g, device=device)
+        x = torch.where(k < 10, ubits(n, 0x00800000 - 1) + 1, x)
+        for kk, v in ((10, 0), (11, 0x80000000), (12, 0x7F800000), (13, 0xFF800000),
+                      (14, 0x7FC12345), (15, 0xFFA54321)):
+            x = torch.where(k == kk, torch.full_like(x, v), x)
+        x = torch.where(k == 16, x | 0x80000000, x)
+        if name == "log1pf":
+            u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+            neg = (-u).to(torch.float32).view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            x = torch.where((k >= 17) & (k < 80), neg, x)
+    x = x & 0xFFFFFFFF
+    x = torch.where(x >= 2**31, x - 2**32, x)
+    return x.to(torch.int32).view(torch.float32)

@@ -283,6 +283,87 @@ def gen_atrig():
     scalar("PI_H", h); scalar("PI_L", l)
     an = [mp.mpf((-1) ** n) / (2 * n + 1) for n in range(20)]
     arr("ATANT_HI", [dd(v)[0] for v in an]); arr("ATANT_LO", [dd(v)[1] for v in an])
+    gen_asin()
+    gen_atan()
+
+
+def gen_atan():
+    """atan by angle subtraction: atan z = A_k + atan((z C_k - S_k)/(C_k + z S_k))
+    for any angle A_k (C, S = cos, sin A_k). Entry k = j + 8*up, up = (z > 1),
+    j = RN(7.49 * min(z, 1/z)) in 0..7: A_j = atan(j/7.49), A_{8+j} = pi/2 - A_j,
+    rounded to 21 bits (one 32-bit word per entry)."""
+    emit("// ---- atan: angle-subtraction table, k = j + 8*up ----")
+    K = mp.mpf("7.49")
+    ang = []
+    for k in range(16):
+        j, up = k % 8, k >= 8
+        th = mp.atan(mp.mpf(j) / K)
+        ang.append(mp.pi / 2 - th if up else th)
+    hv = [hi_word(a) for a in ang]
+    emit("static CR_CONST int ATAN_A_HI[16] = {")
+    emit("    " + ", ".join(str(h if h < 2**31 else h - 2**32) for _, h in hv) + ",")
+    emit("};")
+    arr("ATAN_C", [d(mp.cos(v)) for v, _ in hv])
+    arr("ATAN_S", [d(mp.sin(v)) for v, _ in hv])
+    worst = mp.mpf(0)
+    for i in range(20001):
+        p = mp.mpf(i) / 20000
+        j = int(mp.nint(p * K))
+        worst = max(worst, abs(mp.atan(p) - hv[j][0]))
+    T = mp.tan(worst) * mp.mpf("1.02")
+    report.append(f"atan (angle subtraction) reduced |t| <= {float(T):.5f}")
+    g = lambda s: (mp.atan(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 3
+    cs, _ = chebfit(g, mp.mpf(0), T ** 2, 3)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda t: t + t ** 3 * horner(csd, t * t), mp.atan, -T, T)
+    report.append(f"atan2 poly deg 3 in t^2 (|t| <= {float(T):.4f}): max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("ATANQ2", csd)
+
+
+def hi_word(x):
+    """x rounded to 21 significant bits: a double whose low word is zero."""
+    v = trunc_bits(x, 21)
+    b = int.from_bytes(__import__("struct").pack("<d", v), "little")
+    assert b & 0xFFFFFFFF == 0
+    return v, b >> 32
+
+
+def gen_asin():
+    """asin / acos by angle subtraction without division:
+    asin(|x|) = A_k + asin(|x| cos A_k - s sin A_k), s = sqrt(1 - x^2), and
+    acos(|x|) = B_k + asin(s cos B_k - |x| sin B_k). Entry k = j + 8*up,
+    up = (|x| > s), j = RN(10.5 * min(|x|, s)) in 0..7; the angles are rounded
+    to 21 bits (one 32-bit word per entry) and their sin / cos rounded to
+    binary64, so sin(theta - A_k) is a two-term dot product."""
+    emit("// ---- asin / acos: angle-subtraction tables, k = j + 8*up ----")
+    PI2 = mp.pi / 2
+    A, B = [], []
+    for k in range(16):
+        j, up = k % 8, k >= 8
+        th = mp.asin(mp.mpf(j) / mp.mpf("10.5"))
+        A.append(PI2 - th if up else th)
+        B.append(th if up else PI2 - th)
+    for name, ang in (("ASIN", A), ("ACOS", B)):
+        hv = [hi_word(a) for a in ang]
+        emit(f"static CR_CONST int {name}_A_HI[16] = {{")
+        emit("    " + ", ".join(str(h if h < 2**31 else h - 2**32) for _, h in hv) + ",")
+        emit("};")
+        arr(f"{name}_C", [d(mp.cos(v)) for v, _ in hv])
+        arr(f"{name}_S", [d(mp.sin(v)) for v, _ in hv])
+    # reduced argument bound: |theta - A_k| over the grid (+ rounding slack)
+    worst = mp.mpf(0)
+    for i in range(20001):
+        p = mp.sqrt(mp.mpf(1) / 2) * i / 20000
+        j = int(mp.nint(p * mp.mpf("10.5")))
+        worst = max(worst, abs(mp.asin(p) - mp.asin(mp.mpf(j) / mp.mpf("10.5"))))
+    D = mp.sin(worst) * mp.mpf("1.02")
+    report.append(f"asin reduced |d| <= {float(D):.5f}")
+    g = lambda s: (mp.asin(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else mp.mpf(1) / 6
+    cs, _ = chebfit(g, mp.mpf(0), D ** 2, 3)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda t: t + t ** 3 * horner(csd, t * t), mp.asin, -D, D)
+    report.append(f"asin poly deg 3 in d^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("ASINQ", csd)
 
 
 # ---------------------------------------------------------------- binary64 --

@@ -13,7 +13,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2605_15547_b200 as crvec  # noqa: E402
-from tests.inputs import log_family_input, mixed_f32, trig_input  # noqa: E402
+from tests.inputs import device_input, log_family_input, mixed_f32, trig_input  # noqa: E402
 
 
 def inputs(name, n, dist="config"):
@@ -52,7 +52,7 @@ def main():
     y2 = torch.empty(n, dtype=torch.float32, device="cuda")
     rows = []
     for name in names:
-        x = torch.from_numpy(inputs(name, n, a.dist).view(np.float32)).cuda()
+        x = device_input(name, n, a.dist)
         fid = crvec.FN_IDS[name]
         for _ in range(3):
             L.crvec_eval_f32_dev(fid, x.data_ptr(), y.data_ptr(), y2.data_ptr(), n, a.mode, sp)
