@@ -492,7 +492,7 @@ CR_F RedTrig red_trig_small(double xd) {
 // Payne-Hanek for |x| >= 2^17 (binary32 x = M * 2^(ex-23)):
 // x*16/pi mod 32 from a 32*NW-bit window of 1/pi times the 24-bit M.
 // Returns k mod 32 (of |x|) and the 64-bit signed fraction (units 2^-64),
-// plus (NW >= 6) the next 64 fraction bits for the accurate path.
+// plus the next 64 (NW >= 5) or 59 (NW = 4) fraction bits.
 struct PH {
   int k;
   int64_t f;      // fraction * 2^64, in [-2^63, 2^63)
@@ -524,9 +524,9 @@ CR_F PH payne_hanek(uint32_t xb, const unsigned *words) {
   uint32_t top = L[NW - 1];
   uint32_t kk = top >> 27;
   uint64_t f = ((uint64_t)(top & 0x07FFFFFFu) << 37) | ((uint64_t)L[NW - 2] << 5) | (L[NW - 3] >> 27);
-  uint64_t f2 = 0;
-  if (NW >= 6)
-    f2 = ((uint64_t)(L[NW - 3] & 0x07FFFFFFu) << 37) | ((uint64_t)L[NW - 4] << 5) | (L[NW - 5] >> 27);
+  static_assert(NW >= 4, "window too short");
+  uint64_t f2 = ((uint64_t)(L[NW - 3] & 0x07FFFFFFu) << 37) | ((uint64_t)L[NW - 4] << 5);
+  if constexpr (NW >= 5) f2 |= L[NW - 5] >> 27;
   kk += (uint32_t)(f >> 63);
   return {(int)kk, (int64_t)f, f2};
 }
@@ -587,7 +587,10 @@ CR_F DD red_trig_dd(float x, int &k) {
 // per-lane body it runs.
 CR_F RedTrig ph_reduce(float x, const unsigned *words) {
   uint32_t xb = f2u(x);
-  PH p = payne_hanek<6>(xb & 0x7FFFFFFFu, words);
+  // 128-bit window: x*16/pi has at most ~30 leading zero fraction bits for a
+  // binary32 x, and the window keeps ~99 correct fraction bits (truncating
+  // 1/pi after it perturbs the product by < 2^24 units of its last word).
+  PH p = payne_hanek<4>(xb & 0x7FFFFFFFu, words);
   // 64 + 53 fraction bits: relative accuracy of r even when |r| is tiny.
   double fr = fma_((double)(p.f2 >> 11), 0x1p-53, (double)p.f);
   double r = mul_(fr, PI_16_2M64_H);

@@ -37,6 +37,42 @@ __device__ __forceinline__ void st_stream(float4 *p, float4 v) {
                : "memory");
 }
 
+// Per-lane access unit of the map kernels: VW consecutive floats, one 128-bit
+// (VW = 4) or 256-bit (VW = 8: LDG/STG.E.ENL2.256, new on sm_100) access, so a
+// warp moves 512 B or 1 KiB per instruction.
+template <int VW>
+struct alignas(4 * VW) Vec {
+  float v[VW];
+};
+template <int VW>
+__device__ __forceinline__ Vec<VW> ld_vec(const Vec<VW> *p) {
+  Vec<VW> r;
+  if constexpr (VW == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p));
+  } else {
+    static_assert(VW == 8, "VW");
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+  }
+  return r;
+}
+template <int VW>
+__device__ __forceinline__ void st_vec(Vec<VW> *p, const uint32_t *y) {
+  if constexpr (VW == 4) {
+    asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(y[0]), "r"(y[1]),
+                 "r"(y[2]), "r"(y[3])
+                 : "memory");
+  } else {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(y[0]),
+                 "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7])
+                 : "memory");
+  }
+}
+
 // Accurate path: one lane, double-double evaluation + round_dd. Out of line so
 // the fast path keeps its register budget; reached with probability ~2^-24.
 template <class F, int M>
@@ -55,9 +91,8 @@ __device__ __noinline__ DD slow_dd(float x) {
 // a time by all lanes, and read back by their owners. One pass serves up to 32 big arguments however
 // they are spread over lanes and slots.
 struct PHWarp {
-  float qx[256];
-  int rk[256];
   double rr[256];
+  int qx[256];  // queued x bits, overwritten by the reduced k
 };
 struct PHBlock {
   unsigned words[12];
@@ -84,14 +119,14 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
   int j = base;
 #pragma unroll
   for (int e = 0; e < NE; ++e)
-    if (big[e]) w.qx[j++] = xs[e];
+    if (big[e]) w.qx[j++] = (int)f2u(xs[e]);
   __syncwarp();
   // all lanes reduce the compacted queue, 32 arguments per pass
   for (int b0 = 0; b0 < total; b0 += 32) {
     int i = b0 + lane;
     if (i < total) {
-      RedTrig r = ph_reduce(w.qx[i], sh.words);
-      w.rk[i] = r.k;
+      RedTrig r = ph_reduce(u2f((uint32_t)w.qx[i]), sh.words);
+      w.qx[i] = r.k;
       w.rr[i] = r.r;
     }
   }
@@ -100,7 +135,7 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
 #pragma unroll
   for (int e = 0; e < NE; ++e)
     if (big[e]) {
-      q[e] = RedTrig{w.rk[j], w.rr[j]};
+      q[e] = RedTrig{w.qx[j], w.rr[j]};
       ++j;
     }
   __syncwarp();
@@ -216,77 +251,72 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // (minb; 256 threads per block).
 template <class F>
 struct KernelShape {
-  static constexpr int nv = 2, minb = 3;
+  static constexpr int vw = 4, nv = 2, minb = 3;
 };
-template <> struct KernelShape<FnExp2> { static constexpr int nv = 4, minb = 2; };
-template <> struct KernelShape<FnExp10> { static constexpr int nv = 4, minb = 2; };
-template <> struct KernelShape<FnExp> { static constexpr int nv = 2, minb = 4; };
-template <> struct KernelShape<FnExpm1> { static constexpr int nv = 1, minb = 5; };
-template <> struct KernelShape<FnTanh> { static constexpr int nv = 1, minb = 4; };
-template <> struct KernelShape<FnLog1p> { static constexpr int nv = 2, minb = 4; };
-template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int nv = 1, minb = 4; };
-template <class F>
-struct VecWidth {
-  static constexpr int value = KernelShape<F>::nv;
-};
+template <> struct KernelShape<FnExp2> { static constexpr int vw = 4, nv = 4, minb = 2; };
+template <> struct KernelShape<FnExp10> { static constexpr int vw = 4, nv = 4, minb = 2; };
+template <> struct KernelShape<FnExp> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 1, minb = 5; };
+template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 1, minb = 4; };
+template <> struct KernelShape<FnLog1p> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step
 // into `nxt`, evaluate `cur`, store. Called alternately with the two register
 // buffers swapped, so the double buffer needs no register moves.
-template <class F, int M, int NV>
-__device__ __forceinline__ void map_step(const float4 *__restrict__ x, float4 *__restrict__ y,
-                                         uint32_t n4, uint32_t base, uint32_t stride,
-                                         const float4 (&cur)[NV], float4 (&nxt)[NV],
+template <class F, int M, int VW, int NV>
+__device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> *__restrict__ y,
+                                         uint32_t nv, uint32_t base, uint32_t stride,
+                                         const Vec<VW> (&cur)[NV], Vec<VW> (&nxt)[NV],
                                          const typename F::Regs &R, PHBlock *sh,
                                          unsigned long long *counters) {
-  float xs[4 * NV];
+  float xs[VW * NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t in = base + stride + 32 * k;
-    if (in < n4) nxt[k] = ld_stream(x + in);
-    xs[4 * k] = cur[k].x;
-    xs[4 * k + 1] = cur[k].y;
-    xs[4 * k + 2] = cur[k].z;
-    xs[4 * k + 3] = cur[k].w;
+    if (in < nv) nxt[k] = ld_vec<VW>(x + in);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) xs[VW * k + j] = cur[k].v[j];
   }
-  uint32_t ys[4 * NV];
-  eval_lanes<F, M, 4 * NV>(xs, ys, R, sh, counters);
+  uint32_t ys[VW * NV];
+  eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = base + 32 * k;
-    if (i < n4)
-      st_stream(y + i, make_float4(u2f(ys[4 * k]), u2f(ys[4 * k + 1]), u2f(ys[4 * k + 2]),
-                                   u2f(ys[4 * k + 3])));
+    if (i < nv) st_vec<VW>(y + i, ys + VW * k);
   }
 }
 
 template <class F, int M>
 __global__ void __launch_bounds__(kThreads, KernelShape<F>::minb)
-    k_map_vec(const float4 *__restrict__ x, float4 *__restrict__ y, uint32_t n4,
+    k_map_vec(const float *__restrict__ xf, float *__restrict__ yf, uint32_t nv,
               unsigned long long *counters) {
-  constexpr int NV = VecWidth<F>::value;
+  constexpr int VW = KernelShape<F>::vw, NV = KernelShape<F>::nv;
+  const Vec<VW> *x = reinterpret_cast<const Vec<VW> *>(xf);
+  Vec<VW> *y = reinterpret_cast<Vec<VW> *>(yf);
   PHBlock *sh = ph_storage<F>();
   typename F::Regs R;
   F::load(R);
-  // 32-bit float4 indices (the launcher keeps n4 <= 2^31): one IMAD.WIDE per
-  // address, one compare per access. Each warp handles NV x 32 float4 per
+  // 32-bit vector indices (the launcher keeps nv <= 2^31): one IMAD.WIDE per
+  // address, one compare per access. Each warp handles NV x 32 vectors per
   // step; the trip count is warp-uniform (register-table shuffles need the
   // whole warp).
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * (uint32_t)(kThreads * NV);
   uint32_t base = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 * NV) + lane;
-  float4 va[NV], vb[NV];
+  Vec<VW> va[NV], vb[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    va[k] = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) va[k].v[j] = 1.0f;
     vb[k] = va[k];
-    if (base + 32 * k < n4) va[k] = ld_stream(x + base + 32 * k);
+    if (base + 32 * k < nv) va[k] = ld_vec<VW>(x + base + 32 * k);
   }
-  while (base - lane < n4) {
-    map_step<F, M, NV>(x, y, n4, base, stride, va, vb, R, sh, counters);
+  while (base - lane < nv) {
+    map_step<F, M, VW, NV>(x, y, nv, base, stride, va, vb, R, sh, counters);
     base += stride;
-    if (base - lane >= n4) break;
-    map_step<F, M, NV>(x, y, n4, base, stride, vb, va, R, sh, counters);
+    if (base - lane >= nv) break;
+    map_step<F, M, VW, NV>(x, y, nv, base, stride, vb, va, R, sh, counters);
     base += stride;
   }
 }
@@ -312,10 +342,13 @@ __global__ void __launch_bounds__(kThreads) k_map_scalar(const float *x, float *
 }
 
 // sincosf: one reduction, two outputs (1 in / 2 out = 12 B per element).
+// The rare mask carries the sin slots in bits 0..15 and the cos slots in
+// bits 16..31; one gather pass resolves either kind.
 template <int M, int NE>
 __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s)[NE],
                                              uint32_t (&c)[NE], const FnSin::Regs &R,
                                              PHBlock *sh, unsigned long long *counters) {
+  static_assert(NE <= 16, "mask layout");
   RedTrig q[NE];
   bool big[NE];
   bool anyb = false;
@@ -326,71 +359,89 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
     anyb |= big[e];
   }
   if (__any_sync(kFull, anyb)) coop_payne_hanek<NE>(xs, big, q, *sh);
-  bool fs[NE], fc[NE];
-  Fast a[NE], b[NE];
-  bool rare = false;
+  unsigned mask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    a[e] = FnSin::from_red(xs[e], q[e], R);
-    b[e] = FnCos::from_red(xs[e], q[e], R);
-    s[e] = finish<M>(a[e], fs[e], FnSin::E);
-    c[e] = finish<M>(b[e], fc[e], FnCos::E);
-    rare |= fs[e] | fc[e] | !a[e].main | !b[e].main;
+    const Fast a = FnSin::from_red(xs[e], q[e], R);
+    const Fast b = FnCos::from_red(xs[e], q[e], R);
+    s[e] = f2u(cvt_f32<M>(a.a));
+    c[e] = f2u(cvt_f32<M>(b.a));
+    mask |= (unsigned)((!a.main) | near_boundary(a.a, FnSin::E)) << e;
+    mask |= (unsigned)((!b.main) | near_boundary(b.a, FnCos::E)) << (e + 16);
   }
-  if (__any_sync(kFull, rare)) {
+  if (__any_sync(kFull, mask != 0)) {
     int cnt = 0;
+    do {
+      const unsigned low = mask & (0u - mask);
+      const unsigned slot = (low | (low >> 16)) & 0xFFFFu;
+      const float xe = gather_slot<NE>(xs, slot);
+      uint32_t r = 0;
+      if (low) r = (low >> 16) ? resolve_one<FnCos, M>(xe, cnt) : resolve_one<FnSin, M>(xe, cnt);
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      if (!a[e].main) s[e] = FnSin::special<M>(xs[e]);
-      else if (fs[e]) { s[e] = slow_round<FnSin, M>(xs[e]); ++cnt; }
-      if (!b[e].main) c[e] = FnCos::special<M>(xs[e]);
-      else if (fc[e]) { c[e] = slow_round<FnCos, M>(xs[e]); ++cnt; }
-    }
+      for (int e = 0; e < NE; ++e) {
+        s[e] = (low >> e) & 1u ? r : s[e];
+        c[e] = (low >> (e + 16)) & 1u ? r : c[e];
+      }
+      mask &= ~low;
+    } while (__any_sync(kFull, mask != 0));
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);
   }
 }
 
+template <int M, int NV>
+__device__ __forceinline__ void sincos_step(const float4 *__restrict__ x, float4 *__restrict__ ys,
+                                            float4 *__restrict__ yc, uint32_t n4, uint32_t base,
+                                            uint32_t stride, const float4 (&cur)[NV],
+                                            float4 (&nxt)[NV], const FnSin::Regs &R, PHBlock *sh,
+                                            unsigned long long *counters) {
+  float xs[4 * NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t in = base + stride + 32 * k;
+    if (in < n4) nxt[k] = ld_stream(x + in);
+    xs[4 * k] = cur[k].x;
+    xs[4 * k + 1] = cur[k].y;
+    xs[4 * k + 2] = cur[k].z;
+    xs[4 * k + 3] = cur[k].w;
+  }
+  uint32_t s[4 * NV], c[4 * NV];
+  sincos_lanes<M, 4 * NV>(xs, s, c, R, sh, counters);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t i = base + 32 * k;
+    if (i < n4) {
+      st_stream(ys + i, make_float4(u2f(s[4 * k]), u2f(s[4 * k + 1]), u2f(s[4 * k + 2]), u2f(s[4 * k + 3])));
+      st_stream(yc + i, make_float4(u2f(c[4 * k]), u2f(c[4 * k + 1]), u2f(c[4 * k + 2]), u2f(c[4 * k + 3])));
+    }
+  }
+}
+
+constexpr int kSincosNV = 2, kSincosMinB = 2;
+
 template <int M>
-__global__ void __launch_bounds__(kThreads, 2) k_sincos_vec(const float4 *x, float4 *ys, float4 *yc,
-                                                            uint64_t n4, unsigned long long *counters) {
-  constexpr int NV = 2;
+__global__ void __launch_bounds__(kThreads, kSincosMinB)
+    k_sincos_vec(const float4 *__restrict__ x, float4 *__restrict__ ys, float4 *__restrict__ yc,
+                 uint32_t n4, unsigned long long *counters) {
+  constexpr int NV = kSincosNV;
   PHBlock *sh = ph_storage<FnSin>();
   FnSin::Regs R;
   FnSin::load(R);
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  const uint64_t stride = nwarps * 32 * NV;
-  uint64_t base = warp * 32 * NV;
-  float4 v[NV];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * (uint32_t)(kThreads * NV);
+  uint32_t base = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 * NV) + lane;
+  float4 va[NV], vb[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    uint64_t i = base + 32 * k + lane;
-    v[k] = ld_stream(x + (i < n4 ? i : n4 - 1));
+    va[k] = make_float4(1.f, 1.f, 1.f, 1.f);
+    vb[k] = va[k];
+    if (base + 32 * k < n4) va[k] = ld_stream(x + base + 32 * k);
   }
-  for (; base < n4; base += stride) {
-    float4 nx[NV];
-    float xs[4 * NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      uint64_t in = base + 32 * k + lane + stride;
-      nx[k] = ld_stream(x + (in < n4 ? in : n4 - 1));
-      xs[4 * k] = v[k].x;
-      xs[4 * k + 1] = v[k].y;
-      xs[4 * k + 2] = v[k].z;
-      xs[4 * k + 3] = v[k].w;
-    }
-    uint32_t s[4 * NV], c[4 * NV];
-    sincos_lanes<M, 4 * NV>(xs, s, c, R, sh, counters);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      uint64_t i = base + 32 * k + lane;
-      if (i < n4) {
-        st_stream(ys + i, make_float4(u2f(s[4 * k]), u2f(s[4 * k + 1]), u2f(s[4 * k + 2]), u2f(s[4 * k + 3])));
-        st_stream(yc + i, make_float4(u2f(c[4 * k]), u2f(c[4 * k + 1]), u2f(c[4 * k + 2]), u2f(c[4 * k + 3])));
-      }
-      v[k] = nx[k];
-    }
+  while (base - lane < n4) {
+    sincos_step<M, NV>(x, ys, yc, n4, base, stride, va, vb, R, sh, counters);
+    base += stride;
+    if (base - lane >= n4) break;
+    sincos_step<M, NV>(x, ys, yc, n4, base, stride, vb, va, R, sh, counters);
+    base += stride;
   }
 }
 
@@ -644,20 +695,21 @@ inline unsigned grid_for(uint64_t work_warps32, int maxb) {
 template <class F, int M>
 cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream_t s,
                        unsigned long long *ctr) {
+  constexpr int VW = KernelShape<F>::vw, NV = KernelShape<F>::nv;
   static int mb_vec = max_blocks(k_map_vec<F, M>);
   static int mb_sc = max_blocks(k_map_scalar<F, M>);
-  bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
-  uint64_t n4 = aligned ? n / 4 : 0;
-  // the kernel indexes float4s with 32 bits: launches of at most 2^31 float4s
-  constexpr uint64_t kMaxN4 = uint64_t(1) << 31;
-  for (uint64_t off = 0; off < n4; off += kMaxN4) {
-    uint64_t m = n4 - off < kMaxN4 ? n4 - off : kMaxN4;
-    k_map_vec<F, M><<<grid_for((m + 32 * VecWidth<F>::value - 1) / (32 * VecWidth<F>::value), mb_vec),
-                      kThreads, 0, s>>>((const float4 *)x + off, (float4 *)y + off, (uint32_t)m, ctr);
+  bool aligned = (((uintptr_t)x | (uintptr_t)y) & (4 * VW - 1)) == 0;
+  uint64_t nvec = aligned ? n / VW : 0;
+  // the kernel indexes vectors with 32 bits: launches of at most 2^31 vectors
+  constexpr uint64_t kMaxNV = uint64_t(1) << 31;
+  for (uint64_t off = 0; off < nvec; off += kMaxNV) {
+    uint64_t m = nvec - off < kMaxNV ? nvec - off : kMaxNV;
+    const unsigned g = grid_for((m + 32 * NV - 1) / (32 * NV), mb_vec);
+    k_map_vec<F, M><<<g, kThreads, 0, s>>>(x + VW * off, y + VW * off, (uint32_t)m, ctr);
   }
-  uint64_t rem = n - 4 * n4;
+  uint64_t rem = n - VW * nvec;
   if (rem) {
-    k_map_scalar<F, M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(x + 4 * n4, y + 4 * n4,
+    k_map_scalar<F, M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(x + VW * nvec, y + VW * nvec,
                                                                             rem, ctr);
   }
   return cudaGetLastError();
@@ -670,9 +722,12 @@ cudaError_t launch_sincos(const float *x, float *ys, float *yc, uint64_t n, cuda
   static int mb_sc = max_blocks(k_sincos_scalar<M>);
   bool aligned = (((uintptr_t)x | (uintptr_t)ys | (uintptr_t)yc) & 15) == 0;
   uint64_t n4 = aligned ? n / 4 : 0;
-  if (n4)
-    k_sincos_vec<M><<<grid_for((n4 + 63) / 64, mb_vec), kThreads, 0, s>>>(
-        (const float4 *)x, (float4 *)ys, (float4 *)yc, n4, ctr);
+  constexpr uint64_t kMaxN4 = uint64_t(1) << 31;
+  for (uint64_t off = 0; off < n4; off += kMaxN4) {
+    uint64_t m = n4 - off < kMaxN4 ? n4 - off : kMaxN4;
+    k_sincos_vec<M><<<grid_for((m + 32 * kSincosNV - 1) / (32 * kSincosNV), mb_vec), kThreads, 0, s>>>(
+        (const float4 *)x + off, (float4 *)ys + off, (float4 *)yc + off, (uint32_t)m, ctr);
+  }
   uint64_t rem = n - 4 * n4;
   if (rem)
     k_sincos_scalar<M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(

@@ -83,9 +83,9 @@ def test_kernels_compiled_for_sm100a():
     so = os.path.join(ROOT, "paper_2605_15547_b200", "libcrvec.so")
     out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPK6float4PS3_jPy", so],
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPKfPfjPy", so],
                           capture_output=True, text=True).stdout
-    for op in ("DFMA", "SHFL.IDX", "LDG.E.NA.128", "STG.E.EF.128", "F2F.F32.F64"):
+    for op in ("DFMA", "SHFL.IDX", "LDG.E.NA", "STG.E.EF", "F2F.F32.F64"):
         assert op in sass, op
 
 
