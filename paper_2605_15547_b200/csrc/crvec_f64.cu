@@ -12,12 +12,34 @@ namespace crvec {
 
 constexpr int kT64 = 256;
 constexpr int kW64 = kT64 / 32;
-constexpr int kQ = 128;  // per-warp queue capacity
+// Kernel shape per function (measured, profiles/r01/f64_shapes.txt): double2
+// per lane per step, __launch_bounds__ min blocks per SM, grid waves.
+template <int FN> struct F64Shape;
+template <> struct F64Shape<0> { static constexpr int nv = 1, minb = 4, waves = 4; };  // exp2
+template <> struct F64Shape<1> { static constexpr int nv = 2, minb = 3, waves = 1; };  // log
+constexpr int kF64MaxNV = 2;
+constexpr int kQ = 32 + 32 * 2 * kF64MaxNV;  // per-warp queue capacity: < 32 left + one step
 
 struct F64Queue {
   double x[kQ];
   unsigned long long idx[kQ];
 };
+
+// Shared-memory copy of the function's fast-path tables (exp2: 2 KB, log: 12 KB).
+template <int FN>
+__device__ __forceinline__ void load_tables(F64Tab &T) {
+  if (FN == 0) {
+    for (int i = threadIdx.x; i < 64; i += kT64) {
+      T.ah[i] = EXP2D_A_HI[i]; T.al[i] = EXP2D_A_LO[i];
+      T.bh[i] = EXP2D_B_HI[i]; T.bl[i] = EXP2D_B_LO[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < 512; i += kT64) {
+      T.lc[i] = LOGD5_C[i]; T.llh[i] = LOGD5_LT_HI[i]; T.lll[i] = LOGD5_LT_LO[i];
+    }
+  }
+  __syncthreads();
+}
 
 template <int FN, int M>
 __device__ __noinline__ double accurate(double x, int *und) {
@@ -39,82 +61,126 @@ __device__ __forceinline__ void drain(F64Queue &q, int from, int cnt, double *y,
   if (lane == 0 && m) atomicAdd(ctr + 1, (unsigned long long)__popc(m));
 }
 
-template <int FN, int M>
-__global__ void __launch_bounds__(kT64) k_f64(const double *x, double *y, uint64_t n,
-                                              unsigned long long *ctr) {
-  __shared__ F64Tab T;
-  __shared__ F64Queue Q[kW64];
-  for (int i = threadIdx.x; i < 16; i += kT64) {
-    T.t1h[i] = EXP2D_T1_HI[i]; T.t1l[i] = EXP2D_T1_LO[i];
-    T.t2h[i] = EXP2D_T2_HI[i]; T.t2l[i] = EXP2D_T2_LO[i];
-    T.t3h[i] = EXP2D_T3_HI[i]; T.t3l[i] = EXP2D_T3_LO[i];
-  }
-  for (int i = threadIdx.x; i < 128; i += kT64) {
-    T.lc[i] = LOGD_C[i]; T.llh[i] = LOGD_LT_HI[i]; T.lll[i] = LOGD_LT_LO[i];
-  }
-  __syncthreads();
-  F64Queue &q = Q[threadIdx.x >> 5];
+// One step: NE = 2*NV doubles per lane (NV double2 per lane, 32 lanes apart
+// so each warp access is 512 B contiguous), fast path + round test, stores,
+// then the undecided lanes are appended to the warp's side queue; a full
+// queue (32) is drained by the whole warp on the accurate path.
+template <int FN, int M, int NV>
+__device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2 *__restrict__ y2,
+                                         const double *x, double *y, uint32_t n2, uint64_t n, uint32_t base,
+                                         uint32_t stride, const double2 (&cur)[NV],
+                                         double2 (&nxt)[NV], const F64Tab &T, F64Queue &q,
+                                         int &qn, unsigned long long &nfast,
+                                         unsigned long long *ctr) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t in = base + stride + 32 * k;
+    if (2ull * in + 1 < n) nxt[k] = __ldcs(x2 + in);
+    else if (2ull * in < n) nxt[k].x = x[2ull * in];  // odd n: last slot holds one double
+  }
+  double xv[2 * NV];
+  F64Out r[2 * NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    xv[2 * k] = cur[k].x;
+    xv[2 * k + 1] = cur[k].y;
+  }
+#pragma unroll
+  for (int e = 0; e < 2 * NV; ++e)
+    r[e] = FN == 0 ? exp2d_fast<M>(xv[e], T) : logd_fast<M>(xv[e], T);
+  unsigned und = 0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t i = base + 32 * k;
+    const uint64_t i0 = 2ull * i;
+    if (i0 + 1 < n) {
+      __stcs(y2 + i, make_double2(r[2 * k].y, r[2 * k + 1].y));
+    } else if (i0 < n) {
+      y[i0] = r[2 * k].y;
+    }
+    und |= (unsigned)(i0 < n && !r[2 * k].decided) << (2 * k);
+    und |= (unsigned)(i0 + 1 < n && !r[2 * k + 1].decided) << (2 * k + 1);
+  }
+  // compact undecided lanes into the warp's side queue
+  if (__any_sync(0xffffffffu, und != 0)) {
+#pragma unroll
+    for (int e = 0; e < 2 * NV; ++e) {
+      const bool u = (und >> e) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, u);
+      if (u) {
+        const int p = qn + __popc(m & lt);
+        q.x[p] = xv[e];
+        q.idx[p] = 2ull * (base + 32 * (e >> 1)) + (e & 1);
+      }
+      qn += __popc(m);
+      nfast += __popc(m);
+    }
+    __syncwarp();
+    while (qn >= 32) {  // a full warp of hard lanes: evaluate together
+      drain<FN, M>(q, qn - 32, 32, y, ctr);
+      qn -= 32;
+      __syncwarp();
+    }
+  }
+}
+
+template <int FN, int M>
+__global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *x, double *y, uint64_t n,
+                                                 unsigned long long *ctr) {
+  constexpr int NV = F64Shape<FN>::nv;
+  __shared__ F64Tab T;
+  __shared__ F64Queue Q[kW64];
+  load_tables<FN>(T);
+  F64Queue &q = Q[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31;
   int qn = 0;  // warp-uniform queue length
   unsigned long long nfast = 0;
-  const uint64_t warp = ((uint64_t)blockIdx.x * kT64 + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kT64) >> 5;
-  const uint64_t n2 = (n + 1) / 2;  // double2 slots
-  const bool vec = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
-  // register double buffer: the next slot's two doubles are requested before
-  // this slot is computed
-  auto load2 = [&](uint64_t slot) {
-    uint64_t j = 2 * slot;
-    double2 t = make_double2(1.0, 1.0);
-    if (vec && j + 1 < n) {
-      t = __ldcs((const double2 *)(x + j));
-    } else {
-      if (j < n) t.x = x[j];
-      if (j + 1 < n) t.y = x[j + 1];
-    }
-    return t;
-  };
-  const uint64_t stride = nwarps * 32;
-  double2 cur = load2(warp * 32 + lane);
-  for (uint64_t base = warp * 32; base < n2; base += stride) {
-    uint64_t s = base + lane;
-    uint64_t i0 = 2 * s;
-    double2 nxt = load2(s + stride);
-    double xv[2] = {cur.x, cur.y};
-    cur = nxt;
-    bool v0 = i0 < n, v1 = i0 + 1 < n;
-    F64Out r[2];
+  // 16-byte aligned x / y (the launcher guarantees it; odd n handled per lane)
+  const double2 *x2 = reinterpret_cast<const double2 *>(x);
+  double2 *y2 = reinterpret_cast<double2 *>(y);
+  const uint32_t n2 = (uint32_t)((n + 1) / 2);
+  const uint32_t stride = gridDim.x * (uint32_t)(kT64 * NV);
+  uint32_t base = ((blockIdx.x * kT64 + threadIdx.x) >> 5) * (32 * NV) + lane;
+  double2 va[NV], vb[NV];
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
-      r[e] = FN == 0 ? exp2d_fast<M>(xv[e], T) : logd_fast<M>(xv[e], T);
-    bool und0 = v0 && !r[0].decided, und1 = v1 && !r[1].decided;
-    if (vec && v1) {
-      __stcs((double2 *)(y + i0), make_double2(r[0].y, r[1].y));
-    } else {
-      if (v0) y[i0] = r[0].y;
-      if (v1) y[i0 + 1] = r[1].y;
-    }
-    // compact undecided lanes into the warp's side queue
-    unsigned m0 = __ballot_sync(0xffffffffu, und0);
-    unsigned m1 = __ballot_sync(0xffffffffu, und1);
-    if (m0 | m1) {
-      if (und0) { int p = qn + __popc(m0 & lt); q.x[p] = xv[0]; q.idx[p] = i0; }
-      qn += __popc(m0);
-      if (und1) { int p = qn + __popc(m1 & lt); q.x[p] = xv[1]; q.idx[p] = i0 + 1; }
-      qn += __popc(m1);
-      nfast += __popc(m0) + __popc(m1);
-      __syncwarp();
-      while (qn >= 32) {  // a full warp of hard lanes: evaluate together
-        drain<FN, M>(q, qn - 32, 32, y, ctr);
-        qn -= 32;
-        __syncwarp();
-      }
-    }
+  for (int k = 0; k < NV; ++k) {
+    va[k] = make_double2(1.0, 1.0);
+    vb[k] = va[k];
+    const uint32_t i = base + 32 * k;
+    if (2ull * i + 1 < n) va[k] = __ldcs(x2 + i);
+    else if (2ull * i < n) va[k].x = x[2ull * i];
+  }
+  while (base - lane < n2) {
+    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, nfast, ctr);
+    base += stride;
+    if (base - lane >= n2) break;
+    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, nfast, ctr);
+    base += stride;
   }
   __syncwarp();
   if (qn) drain<FN, M>(q, 0, qn, y, ctr);
   if (lane == 0 && nfast) atomicAdd(ctr, nfast);
+}
+
+// Any alignment: one element per thread (fast path, accurate path inline).
+template <int FN, int M>
+__global__ void __launch_bounds__(kT64) k_f64_scalar(const double *x, double *y, uint64_t n,
+                                                     unsigned long long *ctr) {
+  __shared__ F64Tab T;
+  load_tables<FN>(T);
+  for (uint64_t i = (uint64_t)blockIdx.x * kT64 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kT64) {
+    const double xv = x[i];
+    F64Out r = FN == 0 ? exp2d_fast<M>(xv, T) : logd_fast<M>(xv, T);
+    if (!r.decided) {
+      int und = 0;
+      atomicAdd(ctr, 1ull);
+      r.y = accurate<FN, M>(xv, &und);
+      if (und) atomicAdd(ctr + 1, 1ull);
+    }
+    y[i] = r.y;
+  }
 }
 
 template <int FN, int M>
@@ -127,11 +193,25 @@ cudaError_t launch64(const double *x, double *y, uint64_t n, cudaStream_t s,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_f64<FN, M>, kT64, 0);
     return sms * (per > 0 ? per : 1);
   }();
-  uint64_t slots = (n + 1) / 2;
-  uint64_t blocks = (slots + kT64 - 1) / kT64;
-  if (blocks > (uint64_t)maxb) blocks = maxb;
-  if (!blocks) blocks = 1;
-  k_f64<FN, M><<<(unsigned)blocks, kT64, 0, s>>>(x, y, n, ctr);
+  if (!n) return cudaSuccess;
+  const uintptr_t ax = (uintptr_t)x & 15, ay = (uintptr_t)y & 15;
+  if (ax != ay || (ax & 7)) {  // no common 16-byte alignment: element kernel
+    uint64_t blocks = (n + kT64 - 1) / kT64;
+    if (blocks > (uint64_t)maxb) blocks = maxb;
+    k_f64_scalar<FN, M><<<(unsigned)blocks, kT64, 0, s>>>(x, y, n, ctr);
+    return cudaGetLastError();
+  }
+  uint64_t head = ax ? 1 : 0;  // one element until both are 16-byte aligned
+  if (head) k_f64_scalar<FN, M><<<1, kT64, 0, s>>>(x, y, 1, ctr);
+  // 32-bit double2 slot indices: launches of at most 2^32 doubles
+  constexpr uint64_t kMax = uint64_t(1) << 32;
+  for (uint64_t off = head; off < n; off += kMax) {
+    const uint64_t m = n - off < kMax ? n - off : kMax;
+    constexpr int NV = F64Shape<FN>::nv;
+    uint64_t blocks = ((m + 1) / 2 + kT64 * NV - 1) / (kT64 * NV);
+    if (blocks > F64Shape<FN>::waves * (uint64_t)maxb) blocks = F64Shape<FN>::waves * (uint64_t)maxb;
+    k_f64<FN, M><<<(unsigned)(blocks ? blocks : 1), kT64, 0, s>>>(x + off, y + off, m, ctr);
+  }
   return cudaGetLastError();
 }
 

@@ -286,8 +286,8 @@ CR_F double logd_accurate(double x, int *undecided) {
 
 // --------------------------------------------------------- fast paths ----
 struct F64Tab {
-  double t1h[16], t1l[16], t2h[16], t2l[16], t3h[16], t3l[16];
-  double lc[128], llh[128], lll[128];  // llh: -log(c_i) on the 2^-40 grid
+  double ah[64], al[64], bh[64], bl[64];  // 2^(i/64), 2^(i/4096) as double-doubles
+  double lc[512], llh[512], lll[512];     // c_i (10 bits); -log(c_i): 2^-40 grid + rest
 };
 
 struct F64Out {
@@ -344,6 +344,13 @@ CR_F bool exp2d_main(double x) {
   return a > 0x3C80000000000000ull && a < 0x4090CC0000000000ull;  // 2^-55 < |x| < 1075
 }
 
+// exp2 fast path: x = N + (64 ia + ib)/4096 + R, |R| <= 2^-13 exact;
+// 2^x = 2^N T (1 + p) with T = 2^(ia/64) 2^(ib/4096) (two 64-entry DD tables
+// in shared memory; one product instead of the paper's two over 3 x 16
+// entries, ref: proj/src/kernels_f64.cpp:82-90) and 2^R = 1 + ph + pl,
+// ph = RN(R ln2_hi). Error < 2^-74 relative before the round test; the 2^N
+// scale is an integer add to the exponent field (subnormal results take the
+// accurate path).
 template <int M>
 CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
   if (!exp2d_main(x) || x >= 1024.0) return {exp2d_special<M>(x), true};
@@ -351,62 +358,56 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
   double kd = sub_(t, SHIFTER);
   int k = (int)d2lo(t);
   double R = fma_(kd, -0x1p-12, x);  // exact, |R| <= 2^-13
-  int N = k >> 12, i1 = (k >> 8) & 15, i2 = (k >> 4) & 15, i3 = k & 15;
+  int N = k >> 12, ia = (k >> 6) & 63, ib = k & 63;
   if (R == 0.0 && (k & 4095) == 0) {  // integer x: 2^x exact (normal or subnormal)
     double p = N >= -1022 ? u2d((uint64_t)(N + 1023) << 52) : u2d(1ull << (N + 1074));
     return {p, true};
   }
-  DD Tv = dd_mul(dd_mul(DD{T.t1h[i1], T.t1l[i1]}, DD{T.t2h[i2], T.t2l[i2]}), DD{T.t3h[i3], T.t3l[i3]});
-  double q = fma_(fma_(fma_(fma_(EXP2D_Q[5], R, EXP2D_Q[4]), R, EXP2D_Q[3]), R, EXP2D_Q[2]), R,
-                  EXP2D_Q[1]);
-  q = fma_(q, R, EXP2D_Q[0]);
-  // 2^R = 1 + p, p = ph + pl: ph = RN(R ln2_hi) with its exact error folded
-  // into pl together with R ln2_lo and R^2 q(R) (|pl| ~ 2^-53 |p|).
+  // T = A B as an unnormalised DD (|Tl| < 2^-51 |Th|)
+  double ah = T.ah[ia], alo = T.al[ia], bh = T.bh[ib], blo = T.bl[ib];
+  double Th = mul_(ah, bh);
+  double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
+  double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
   DD lin = two_prod(R, LN2D_H);
-  double pl = add_(lin.lo, fma_(R, LN2D_L, mul_(mul_(R, R), q)));
-  // V = T (1 + p) = T.hi + T.hi ph + [T.lo + T.hi pl + T.lo ph], T.hi ph exact
-  DD a = two_prod(Tv.hi, lin.hi);
-  DD v = fast_two_sum(Tv.hi, a.hi);
-  double lo = add_(add_(v.lo, a.lo), fma_(Tv.hi, pl, fma_(Tv.lo, lin.hi, Tv.lo)));
+  double pl = fma_(mul_(R, R), q, fma_(R, LN2D_L, lin.lo));
+  // V = T (1 + p) = Th + Th ph + [Tl + Th pl + Tl ph], Th ph exact
+  DD a = two_prod(Th, lin.hi);
+  DD v = fast_two_sum(Th, a.hi);
+  double lo = add_(add_(v.lo, a.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
   DD V = fast_two_sum(v.hi, lo);
   F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
   if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
-  // scale by 2^N (exact for normal results; 2^1024 overflow only when rounding to 2)
-  r.y = mul_(mul_(r.y, u2d((uint64_t)((N >> 1) + 1023) << 52)),
-             u2d((uint64_t)((N - (N >> 1)) + 1023) << 52));
+  // y in [1, 2]: the exponent add is exact, 2 * 2^1023 correctly gives +Inf
+  r.y = hilo2d(d2hi(r.y) + (N << 20), d2lo(r.y));
   return r;
 }
 
+// log fast path: x = 2^e m, m in [0.75, 1.5), 512 bins (the paper's 128,
+// ref: proj/src/kernels_f64.cpp:102-124, refined so the r^3 term needs no
+// double-double): r = m c_i - 1 exact (c_i has 10 bits, |r| < 2^-9.4),
+// log x = e ln2 - log c_i + r - r^2/2 + r^3 P(r), P of degree 6.
 template <int M>
 CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   int h = d2hi(xs);
   int hh = h - 0x3FE80000;
   int e = (hh >> 20) + eadj;
-  int i = (hh >> 13) & 127;
+  int i = (hh >> 11) & 511;
   double m = hilo2d(h - ((hh >> 20) << 20), d2lo(xs));
-  // r = m c - 1 is exact: c has 7 significant bits, m 53, |r| < 2^-7
-  // (ref: proj/src/kernels_f64.cpp:298-300, "exact or near-exact by construction")
-  double r = fma_(m, T.lc[i], -1.0);
-  DD s = two_prod(r, r);                       // r^2 exact
-  DD u = two_prod(r, s.hi);                    // r^3 ~ u.hi + (u.lo + r s.lo)
-  double ul = fma_(r, s.lo, u.lo);
-  double c3h = mul_(u.hi, THIRD_H);            // r^3 / 3 as c3h + c3l (~2^-100)
-  double c3l = fma_(u.hi, THIRD_H, -c3h) + fma_(ul, THIRD_H, mul_(u.hi, THIRD_L));
-  double qt = LOGD_TAIL[8];
-  for (int n = 7; n >= 0; --n) qt = fma_(qt, r, LOGD_TAIL[n]);
-  double tail = mul_(mul_(s.hi, s.hi), qt);    // r^4 (-1/4 + r/5 - ...), rel 2^-52
-  DD a = fast_two_sum(r, -0.5 * s.hi);         // |r| > |r^2/2|
-  DD b = fast_two_sum(a.hi, c3h);
-  double small = add_(add_(a.lo, b.lo), add_(fma_(-0.5, s.lo, c3l), tail));
+  double r = fma_(m, T.lc[i], -1.0);               // exact
+  DD s = two_prod(r, r);                          // r^2 exact
+  const double *P = LOGD5_P;
+  double p = fma_(fma_(fma_(fma_(fma_(fma_(P[6], r, P[5]), r, P[4]), r, P[3]), r, P[2]), r, P[1]), r, P[0]);
+  double small = mul_(mul_(r, s.hi), p);          // r^3 P(r), relative 2^-81 of r
+  DD a = fast_two_sum(r, -0.5 * s.hi);            // |r| > |r^2/2|
   // e ln2 + L: the high parts add exactly (both on the 2^-40 grid)
   double ed = i2d(e);
   double th = fma_(ed, LN2_HD, T.llh[i]);
   double tl = fma_(ed, LN2_LD, T.lll[i]);
-  DD v = two_sum(th, b.hi);
-  DD V = fast_two_sum(v.hi, add_(add_(v.lo, tl), small));
+  DD v = two_sum(th, a.hi);
+  double lo = add_(add_(v.lo, tl), add_(fma_(-0.5, s.lo, a.lo), small));
+  DD V = fast_two_sum(v.hi, lo);
   return round_test64<M>(V.hi, V.lo, EPS_LOGD * dabs(V.hi));
 }
-
 
 // Lanes outside log's main range (positive normal, x != 1): NaN, +-0, x < 0,
 // +Inf, 1, and subnormals (scaled by 2^54 into the main computation).

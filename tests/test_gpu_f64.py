@@ -137,6 +137,29 @@ def test_sizes_alignment_inplace_f64(cuda, oracle, n):
     assert (v.cpu().numpy().view(np.uint64) == want).all()
 
 
+@pytest.mark.parametrize("n", [1, 5, 4097])
+def test_relative_misalignment_f64(cuda, oracle, n):
+    """x 16-byte aligned, y 8-byte aligned (and the reverse): element kernel;
+    odd sizes exercise the half-filled last double2 slot of the vector kernel."""
+    import ctypes
+    rng = np.random.default_rng(100 + n)
+    x = rng.uniform(-30, 30, n)
+    want = oracle.f64("exp2", x.view(np.uint64), 2)
+    L = crvec.lib()
+    s = ctypes.c_void_p(cuda.cuda.current_stream().cuda_stream)
+    xa = cuda.from_numpy(x).cuda()
+    yb = cuda.zeros(n + 1, dtype=cuda.float64, device="cuda")
+    assert L.crvec_exp2_dev(xa.data_ptr(), yb[1:].data_ptr(), n, 2, s) == 0
+    assert (yb[1:].cpu().numpy().view(np.uint64) == want).all()
+    xb = cuda.zeros(n + 1, dtype=cuda.float64, device="cuda")
+    xb[1:] = xa
+    ya = cuda.zeros(n, dtype=cuda.float64, device="cuda")
+    assert L.crvec_exp2_dev(xb[1:].data_ptr(), ya.data_ptr(), n, 2, s) == 0
+    assert (ya.cpu().numpy().view(np.uint64) == want).all()
+    assert L.crvec_exp2_dev(xa.data_ptr(), ya.data_ptr(), n, 2, s) == 0  # aligned, odd n
+    assert (ya.cpu().numpy().view(np.uint64) == want).all()
+
+
 def test_concurrent_host_callers(cuda, oracle):
     """Host-pointer calls from several threads share the staging workspace safely."""
     import threading

@@ -8,10 +8,9 @@ static F64Tab T;
 static void init() {
   static bool done = false;
   if (done) return;
-  std::memcpy(T.t1h, EXP2D_T1_HI, 128); std::memcpy(T.t1l, EXP2D_T1_LO, 128);
-  std::memcpy(T.t2h, EXP2D_T2_HI, 128); std::memcpy(T.t2l, EXP2D_T2_LO, 128);
-  std::memcpy(T.t3h, EXP2D_T3_HI, 128); std::memcpy(T.t3l, EXP2D_T3_LO, 128);
-  std::memcpy(T.lc, LOGD_C, 1024); std::memcpy(T.llh, LOGD_LT_HI, 1024); std::memcpy(T.lll, LOGD_LT_LO, 1024);
+  std::memcpy(T.ah, EXP2D_A_HI, 512); std::memcpy(T.al, EXP2D_A_LO, 512);
+  std::memcpy(T.bh, EXP2D_B_HI, 512); std::memcpy(T.bl, EXP2D_B_LO, 512);
+  std::memcpy(T.lc, LOGD5_C, 4096); std::memcpy(T.llh, LOGD5_LT_HI, 4096); std::memcpy(T.lll, LOGD5_LT_LO, 4096);
   done = true;
 }
 template <int M>

@@ -379,6 +379,14 @@ def gen_f64():
     # 2^R = 1 + R ln2 + R^2 q(R), q Taylor (|R ln2| <= 2^-13.5, truncation < 2^-106)
     q = [LN2 ** n / mp.factorial(n) for n in range(2, 8)]
     arr("EXP2D_Q", [d(c) for c in q])
+    # fast path: x = N + (ia*64 + ib)/4096 + R, two 64-entry DD tables, and a
+    # degree-5 Taylor tail (R^6 term < 2^-84 relative for |R| <= 2^-13)
+    emit("// ---- binary64 exp2 fast path: 2^(ia/64) * 2^(ib/4096), 64-entry DD tables ----")
+    for nm, den in (("A", 64), ("B", 4096)):
+        T = [mp.mpf(2) ** (mp.mpf(j) / den) for j in range(64)]
+        arr(f"EXP2D_{nm}_HI", [dd(t)[0] for t in T])
+        arr(f"EXP2D_{nm}_LO", [dd(t)[1] for t in T])
+    arr("EXP2D_Q4", [d(LN2 ** n / mp.factorial(n)) for n in range(2, 6)])
     h, l = dd(LN2)
     scalar("LN2D_H", h); scalar("LN2D_L", l)
     emit("// ---- binary64 log: m in [0.75, 1.5), 128 bins, c_i = 1/mid (7 bits) ----")
@@ -400,6 +408,26 @@ def gen_f64():
     Lt = [mp.nint(v * mp.mpf(2) ** 40) / mp.mpf(2) ** 40 for v in Ls]
     arr("LOGD_LT_HI", [d(v) for v in Lt])
     arr("LOGD_LT_LO", [d(v - t) for v, t in zip(Ls, Lt)])
+    # fast path (B200): 512 bins, c_i = 1/mid to 10 bits (r = m c_i - 1 exact,
+    # |r| < 2^-9.4, 53 bits), -log c_i split on the 2^-40 grid, degree-6 tail
+    emit("// ---- binary64 log fast path: 512 bins, |r| < 2^-9.4 ----")
+    cs5, L5 = [], []
+    for i in range(512):
+        if i < 256:
+            a = mp.mpf("0.75") + mp.mpf(i) / 1024
+            b = a + mp.mpf(1) / 1024
+        else:
+            a = 1 + mp.mpf(i - 256) / 512
+            b = a + mp.mpf(1) / 512
+        c = mp.mpf(1) if i in (255, 256) else mp.mpf(trunc_bits(2 / (a + b), 10))
+        cs5.append(float(c))
+        L5.append(-mp.log(c))
+    arr("LOGD5_C", cs5)
+    Lt5 = [mp.nint(v * mp.mpf(2) ** 40) / mp.mpf(2) ** 40 for v in L5]
+    arr("LOGD5_LT_HI", [d(v) for v in Lt5])
+    arr("LOGD5_LT_LO", [d(v - t) for v, t in zip(L5, Lt5)])
+    # log1p(r) = r - r^2/2 + r^3 P(r), P(r) = 1/3 - r/4 + ... + r^6/9
+    arr("LOGD5_P", [d(mp.mpf((-1) ** n) / (n + 3)) for n in range(7)])
     h, m, l = split3(LN2, 40, 40)
     scalar("LN2_HD", h)
     scalar("LN2_LD", d(LN2 - h))
