@@ -227,14 +227,13 @@ struct HypParts {
 CR_F HypParts hyp_parts(double ax, double tab) {
   RedExp q = red_exp(ax);
   int kp = q.k, km = -q.k;
-  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp), kp >> 4);
-  double Em = scale2(CR_TAB(tab, EXP2J_HI, km), km >> 4);
+  // e^(+-a)/2: the halving folds into the integer exponent add
+  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp), (kp >> 4) - 1);
+  double Em = scale2(CR_TAB(tab, EXP2J_HI, km), (km >> 4) - 1);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ[2], s, SINHQ[1]), s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(fma_(COSHQ[2], s, COSHQ[1]), s, COSHQ[0]), 1.0);
-  double Sa = mul_(sub_(Ep, Em), 0.5);
-  double Ca = mul_(add_(Ep, Em), 0.5);
-  return {Sa, Ca, sr, cr};
+  return {sub_(Ep, Em), add_(Ep, Em), sr, cr};
 }
 struct HypDD {
   DD Sa, Ca, sr, cr;
