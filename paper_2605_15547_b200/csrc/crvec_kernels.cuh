@@ -245,8 +245,8 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // ------------------------------------------------------------ map kernels ----
 // 4 elements (one float4) per lane per iteration; the loop trip count is
 // warp-uniform so the register-table shuffles always see a full warp.
-// Kernel shape per function, chosen by measurement (tools/gpu_shapes.sh over
-// tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw1.txt): float4s
+// Kernel shape per function, chosen by measurement (tools/gpu_ab2.sh over
+// tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw2.txt): float4s
 // per lane per step (nv) and the __launch_bounds__ min-blocks register cap
 // (minb; 256 threads per block).
 template <class F>
@@ -256,9 +256,12 @@ struct KernelShape {
 template <> struct KernelShape<FnExp2> { static constexpr int vw = 4, nv = 4, minb = 2; };
 template <> struct KernelShape<FnExp10> { static constexpr int vw = 4, nv = 4, minb = 2; };
 template <> struct KernelShape<FnExp> { static constexpr int vw = 4, nv = 2, minb = 4; };
-template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 1, minb = 5; };
-template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 1, minb = 4; };
+template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnLog10> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnAtan> { static constexpr int vw = 4, nv = 2, minb = 2; };
+template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 4, nv = 2, minb = 4; };
 template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step

@@ -8,9 +8,14 @@ for s in $1; do
 import re, sys
 p, nv, mb = sys.argv[1], sys.argv[2], sys.argv[3]
 s = open(p).read()
-s = re.sub(r"static constexpr int nv = \d+, minb = \d+;", f"static constexpr int nv = {nv}, minb = {mb};", s)
+s = re.sub(r"static constexpr int vw = 4, nv = \d+, minb = \d+;", f"static constexpr int vw = 4, nv = {nv}, minb = {mb};", s)
 open(p, "w").write(s)
 PY
-  python -m paper_2605_15547_b200.build --variant s$nv$mb $d 2>&1 | tail -1 &
+done
+for s in $1; do
+  nv=${s%:*}; mb=${s#*:}
+  python -m paper_2605_15547_b200.build --variant s$nv$mb /tmp/var/s$nv$mb > /tmp/var/s$nv$mb.log 2>&1 &
 done
 wait
+for s in $1; do nv=${s%:*}; mb=${s#*:}; tail -n 1 /tmp/var/s$nv$mb.log; done
+rm -rf paper_2605_15547_b200/variants/_build_*
