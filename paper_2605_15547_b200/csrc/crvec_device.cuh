@@ -49,6 +49,14 @@ CR_F double add_(double a, double b) { return __dadd_rn(a, b); }
 CR_F double sub_(double a, double b) { return __dsub_rn(a, b); }
 CR_F double mul_(double a, double b) { return __dmul_rn(a, b); }
 CR_F double i2d(int i) { return __int2double_rn(i); }
+// a + b rounded in mode M (one DADD with a static rounding modifier)
+template <int M>
+CR_F double add_M(double a, double b) {
+  if (M == RNE) return __dadd_rn(a, b);
+  if (M == RZ) return __dadd_rz(a, b);
+  if (M == RU) return __dadd_ru(a, b);
+  return __dadd_rd(a, b);
+}
 CR_F double f2d(float f) { return (double)f; }
 CR_F double dabs(double a) { return fabs(a); }
 CR_F float fabs_(float a) { return fabsf(a); }
@@ -90,6 +98,16 @@ CR_F double add_(double a, double b) { volatile double r = a + b; return r; }
 CR_F double sub_(double a, double b) { volatile double r = a - b; return r; }
 CR_F double mul_(double a, double b) { volatile double r = a * b; return r; }
 CR_F double i2d(int i) { return (double)i; }
+template <int M>
+CR_F double add_M(double a, double b) {
+  double s = add_(a, b), bb = sub_(s, a);
+  double e = add_(sub_(a, sub_(s, bb)), sub_(b, bb));  // a + b = s + e exactly
+  if (M == RNE || e == 0.0) return s;
+  if (M == RZ && (e > 0) != (s > 0)) return std::nextafter(s, 0.0);
+  if (M == RU && e > 0) return std::nextafter(s, INFINITY);
+  if (M == RD && e < 0) return std::nextafter(s, -INFINITY);
+  return s;
+}
 CR_F double f2d(float f) { return (double)f; }
 CR_F double dabs(double a) { return std::fabs(a); }
 CR_F float fabs_(float a) { return std::fabs(a); }

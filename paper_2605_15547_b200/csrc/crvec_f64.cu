@@ -47,18 +47,29 @@ __device__ __noinline__ double accurate(double x, int *und) {
 }
 
 // Drain `cnt` (<= 32) queue entries starting at `from`: one entry per lane.
+// The entry is first re-run through the rule-complete fast path (specials,
+// exact integers, subnormal arguments); what it cannot decide goes to the
+// accurate path. ctr[0] counts lanes sent to the accurate path, ctr[1] the
+// ones it could not decide either.
 template <int FN, int M>
-__device__ __forceinline__ void drain(F64Queue &q, int from, int cnt, double *y,
+__device__ __forceinline__ void drain(F64Queue &q, int from, int cnt, const F64Tab &T, double *y,
                                       unsigned long long *ctr) {
   int lane = threadIdx.x & 31;
   int und = 0;
+  bool acc = false;
   if (lane < cnt) {
     double xv = q.x[from + lane];
     unsigned long long i = q.idx[from + lane];
-    y[i] = accurate<FN, M>(xv, &und);
+    F64Out r = FN == 0 ? exp2d_fast<M>(xv, T) : logd_fast<M>(xv, T);
+    if (!r.decided) {
+      acc = true;
+      r.y = accurate<FN, M>(xv, &und);
+    }
+    y[i] = r.y;
   }
-  unsigned m = __ballot_sync(0xffffffffu, und);
-  if (lane == 0 && m) atomicAdd(ctr + 1, (unsigned long long)__popc(m));
+  unsigned ma = __ballot_sync(0xffffffffu, acc), mu = __ballot_sync(0xffffffffu, und);
+  if (lane == 0 && ma) atomicAdd(ctr, (unsigned long long)__popc(ma));
+  if (lane == 0 && mu) atomicAdd(ctr + 1, (unsigned long long)__popc(mu));
 }
 
 // One step: NE = 2*NV doubles per lane (NV double2 per lane, 32 lanes apart
@@ -70,7 +81,7 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
                                          const double *x, double *y, uint32_t n2, uint64_t n, uint32_t base,
                                          uint32_t stride, const double2 (&cur)[NV],
                                          double2 (&nxt)[NV], const F64Tab &T, F64Queue &q,
-                                         int &qn, unsigned long long &nfast,
+                                         int &qn,
                                          unsigned long long *ctr) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -89,7 +100,7 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
   }
 #pragma unroll
   for (int e = 0; e < 2 * NV; ++e)
-    r[e] = FN == 0 ? exp2d_fast<M>(xv[e], T) : logd_fast<M>(xv[e], T);
+    r[e] = FN == 0 ? exp2d_main_path<M>(xv[e], T) : logd_main_path<M>(xv[e], T);
   unsigned und = 0;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -115,11 +126,10 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
         q.idx[p] = 2ull * (base + 32 * (e >> 1)) + (e & 1);
       }
       qn += __popc(m);
-      nfast += __popc(m);
     }
     __syncwarp();
     while (qn >= 32) {  // a full warp of hard lanes: evaluate together
-      drain<FN, M>(q, qn - 32, 32, y, ctr);
+      drain<FN, M>(q, qn - 32, 32, T, y, ctr);
       qn -= 32;
       __syncwarp();
     }
@@ -136,7 +146,6 @@ __global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *
   F64Queue &q = Q[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   int qn = 0;  // warp-uniform queue length
-  unsigned long long nfast = 0;
   // 16-byte aligned x / y (the launcher guarantees it; odd n handled per lane)
   const double2 *x2 = reinterpret_cast<const double2 *>(x);
   double2 *y2 = reinterpret_cast<double2 *>(y);
@@ -153,15 +162,14 @@ __global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *
     else if (2ull * i < n) va[k].x = x[2ull * i];
   }
   while (base - lane < n2) {
-    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, nfast, ctr);
+    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, ctr);
     base += stride;
     if (base - lane >= n2) break;
-    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, nfast, ctr);
+    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, ctr);
     base += stride;
   }
   __syncwarp();
-  if (qn) drain<FN, M>(q, 0, qn, y, ctr);
-  if (lane == 0 && nfast) atomicAdd(ctr, nfast);
+  if (qn) drain<FN, M>(q, 0, qn, T, y, ctr);
 }
 
 // Any alignment: one element per thread (fast path, accurate path inline).

@@ -295,30 +295,16 @@ struct F64Out {
   bool decided;
 };
 
-// Round test (ref: proj/src/kernels_f64.cpp:63-76) for a normalized DD
-// v = h + l (|l| <= ulp(h)/2) with absolute error bound b.
+// Round test (ref: proj/src/kernels_f64.cpp:63-76): the DD value h + l with
+// absolute error bound b is decided in mode M iff both ends of the enclosure,
+// h + (l +- b), round to the same binary64 - two DADDs with the static
+// rounding modifier, so binade edges, ties and the directed modes need no
+// case analysis (|l| <= ulp(h) and b << |l| rounding error are not needed:
+// l +- b is computed in RN and b carries the margin).
 template <int M>
 CR_F F64Out round_test64(double h, double l, double b) {
-  uint64_t hb = d2u(h);
-  int eh = (int)((hb >> 52) & 0x7FF);
-  bool pow2 = (hb & 0xFFFFFFFFFFFFFull) == 0;
-  double half_ulp = u2d((uint64_t)(eh - 53 > 0 ? eh - 53 : 1) << 52);  // 2^(exp(h)-53)
-  double al = dabs(l);
-  if (M == RNE) {
-    double lim = (pow2 && ((l < 0) != (h < 0))) ? half_ulp * 0.5 : half_ulp;
-    return {h, add_(al, b) < lim};
-  }
-  bool dec = al > b;
-  bool lpos = l > 0, hpos = h > 0;
-  uint64_t r = hb;
-  if (M == RZ) {
-    if (lpos != hpos) r = hb - 1;
-  } else if (M == RU) {
-    if (lpos) r = hpos ? hb + 1 : hb - 1;
-  } else {
-    if (!lpos) r = hpos ? hb - 1 : hb + 1;
-  }
-  return {u2d(r), dec};
+  const double y1 = add_M<M>(h, add_(l, b)), y2 = add_M<M>(h, sub_(l, b));
+  return {y1, y1 == y2};
 }
 
 constexpr double EPS_EXP2D = 0x1p-74;
@@ -386,6 +372,35 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
 // ref: proj/src/kernels_f64.cpp:102-124, refined so the r^3 term needs no
 // double-double): r = m c_i - 1 exact (c_i has 10 bits, |r| < 2^-9.4),
 // log x = e ln2 - log c_i + r - r^2/2 + r^3 P(r), P of degree 6.
+// Vector-kernel form: no special-value branches. Lanes outside the normal-
+// result range, and integer x (exact 2^N), are returned undecided and resolved
+// by the warp's side-queue drain, which runs exp2d_fast (rules) first.
+template <int M>
+CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
+  const uint64_t a = d2u(x) & 0x7FFFFFFFFFFFFFFFull;
+  const bool ok = a > 0x3C80000000000000ull && x < 1024.0 && x >= -1022.0;  // 2^-55 < |x|
+  const double xs = ok ? x : 0.5;
+  double t = fma_(xs, 4096.0, SHIFTER);
+  double kd = sub_(t, SHIFTER);
+  int k = (int)d2lo(t);
+  double R = fma_(kd, -0x1p-12, xs);  // exact, |R| <= 2^-13
+  int N = k >> 12, ia = (k >> 6) & 63, ib = k & 63;
+  double ah = T.ah[ia], alo = T.al[ia], bh = T.bh[ib], blo = T.bl[ib];
+  double Th = mul_(ah, bh);
+  double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
+  double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
+  DD lin = two_prod(R, LN2D_H);
+  double pl = fma_(mul_(R, R), q, fma_(R, LN2D_L, lin.lo));
+  DD aa = two_prod(Th, lin.hi);
+  DD v = fast_two_sum(Th, aa.hi);
+  double lo = add_(add_(v.lo, aa.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
+  DD V = fast_two_sum(v.hi, lo);
+  F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
+  r.decided = r.decided && ok && !(R == 0.0 && (k & 4095) == 0);
+  r.y = hilo2d(d2hi(r.y) + (N << 20), d2lo(r.y));
+  return r;
+}
+
 template <int M>
 CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   int h = d2hi(xs);
@@ -420,6 +435,15 @@ CR_F F64Out logd_special(double x, const F64Tab &T) {
   if (x == INFINITY) return {INFINITY, true};
   if (x == 1.0) return {0.0, true};
   return logd_core<M>(x * 0x1p54, -54, T);  // subnormal
+}
+
+template <int M>
+CR_F F64Out logd_main_path(double x, const F64Tab &T) {
+  const uint64_t xb = d2u(x);
+  const bool ok = xb - 0x0010000000000000ull < 0x7FE0000000000000ull && x != 1.0;  // positive normal
+  F64Out r = logd_core<M>(ok ? x : 2.0, 0, T);
+  r.decided = r.decided && ok;
+  return r;
 }
 
 template <int M>

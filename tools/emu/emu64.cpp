@@ -15,7 +15,10 @@ static void init() {
 }
 template <int M>
 static double one(int fn, double x, int force, uint64_t *st) {
-  F64Out r = fn == 0 ? exp2d_fast<M>(x, T) : logd_fast<M>(x, T);
+  // the vector kernel's order: branch-free main path, then (drain) the
+  // rule-complete fast path, then the accurate path
+  F64Out r = fn == 0 ? exp2d_main_path<M>(x, T) : logd_main_path<M>(x, T);
+  if (!r.decided) r = fn == 0 ? exp2d_fast<M>(x, T) : logd_fast<M>(x, T);
   if (!r.decided || (force && !(x != x) && r.decided == true && force == 2)) {
     ++st[0];
     int und = 0;
