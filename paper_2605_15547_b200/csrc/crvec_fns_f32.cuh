@@ -621,6 +621,16 @@ struct FnTrig {
   CR_F static bool in_main(uint32_t xb) {
     return in_range(xb << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u);
   }
+  // sin and cos from one reduction with one set of table shuffles (shuffles
+  // are not common-subexpression eliminated, so sincosf must share them).
+  CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
+    double s = mul_(q.r, q.r);
+    double sr = sin_r(q.r, s), cr = cos_r(s);
+    double Sk = sin16(R.t, q.k), Ck = sin16(R.t, q.k + 8);
+    const uint32_t xb = f2u(x);
+    fs = Fast{fma_(Sk, cr, mul_(Ck, sr)), FnTrig<0>::in_main(xb)};
+    fc = Fast{fma_(Ck, cr, -mul_(Sk, sr)), FnTrig<1>::in_main(xb)};
+  }
   CR_F static bool is_big(float x) {
     uint32_t az = f2u(x) << 1;
     return az >= (0x48000000u << 1) && az < 0xFF000000u;  // 2^17 <= |x| < inf

@@ -365,8 +365,8 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
   unsigned mask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const Fast a = FnSin::from_red(xs[e], q[e], R);
-    const Fast b = FnCos::from_red(xs[e], q[e], R);
+    Fast a, b;
+    FnSin::sincos_from_red(xs[e], q[e], R, a, b);
     s[e] = f2u(cvt_f32<M>(a.a));
     c[e] = f2u(cvt_f32<M>(b.a));
     mask |= (unsigned)((!a.main) | near_boundary(a.a, FnSin::E)) << e;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void sincos_step(const float4 *__restrict__ x, float4
   }
 }
 
-constexpr int kSincosNV = 2, kSincosMinB = 2;
+constexpr int kSincosNV = 2, kSincosMinB = 3;
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, kSincosMinB)
@@ -593,8 +593,8 @@ __global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, ui
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t xb = pb + e;
-      Fast a = FnSin::from_red(xs[e], q[e], R);
-      Fast b = FnCos::from_red(xs[e], q[e], R);
+      Fast a, b;
+      FnSin::sincos_from_red(xs[e], q[e], R, a, b);
       uint32_t ys[4], yc[4];
       bool fs, fc;
       finish4<FnSin>(xs[e], a, ys, fs);
