@@ -534,14 +534,6 @@ CR_F double sin_r(double r, double s) {
   return fma_(mul_(r, s), fma_(fma_(SINQ[2], s, SINQ[1]), s, SINQ[0]), r);
 }
 CR_F double cos_r(double s) { return fma_(s, fma_(fma_(COSQ[2], s, COSQ[1]), s, COSQ[0]), 1.0); }
-// sin(k pi/16) for any k: entry k mod 16 (shfl takes the source lane mod 32
-// and the table is replicated in both half-warps) with the sign of k & 16
-// flipped into the high word by one XOR.
-CR_F double sin16(double tab, int k) {
-  double v = CR_TAB(tab, SIN16_HI, k);
-  return hilo2d(d2hi(v) ^ ((k << 27) & (int)0x80000000), d2lo(v));
-}
-
 // DD sin/cos of r (|r| <= pi/32), Taylor to r^23.
 CR_F void sincos_r_dd(DD r, DD &sr, DD &cr) {
   DD s = dd_mul(r, r);
@@ -598,23 +590,30 @@ CR_F RedTrig ph_reduce(float x, const unsigned *words) {
   return {k, r};
 }
 
+// Two register tables: sin(j pi/16) and cos(j pi/16), j = k mod 16. With
+// m = bit 4 of k, sin(x) = (-1)^m (S_j cos r + C_j sin r) and cos(x) =
+// (-1)^m (C_j cos r - S_j sin r): one sign flip of the result (none for tan).
 struct TrigRegs {
-  double t;
+  double s, c;
 };
+CR_F double flip_k16(double v, int k) { return hilo2d(d2hi(v) ^ ((k << 27) & (int)0x80000000), d2lo(v)); }
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
   static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
   static constexpr bool kBigArg = true;
   using Regs = TrigRegs;
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(SIN16_HI); }
+  CR_F static void load(Regs &R) {
+    R.s = CR_TAB_LOAD(SIN16_HI);
+    R.c = CR_TAB_LOAD(COS16_HI);
+  }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    double Sk = sin16(R.t, q.k), Ck = sin16(R.t, q.k + 8);
+    double Sj = CR_TAB(R.s, SIN16_HI, q.k), Cj = CR_TAB(R.c, COS16_HI, q.k);
     double a;
-    if (WHICH == 0) a = fma_(Sk, cr, mul_(Ck, sr));
-    else if (WHICH == 1) a = fma_(Ck, cr, -mul_(Sk, sr));
-    else a = div_fast(fma_(Sk, cr, mul_(Ck, sr)), fma_(Ck, cr, -mul_(Sk, sr)));
+    if (WHICH == 0) a = flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k);
+    else if (WHICH == 1) a = flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k);
+    else a = div_fast(fma_(Sj, cr, mul_(Cj, sr)), fma_(Cj, cr, -mul_(Sj, sr)));
     // main: tiny threshold < |x| < inf (sin 2^-12, cos/tan 2^-13)
     return Fast{a, in_main(f2u(x))};
   }
@@ -626,10 +625,10 @@ struct FnTrig {
   CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    double Sk = sin16(R.t, q.k), Ck = sin16(R.t, q.k + 8);
+    double Sj = CR_TAB(R.s, SIN16_HI, q.k), Cj = CR_TAB(R.c, COS16_HI, q.k);
     const uint32_t xb = f2u(x);
-    fs = Fast{fma_(Sk, cr, mul_(Ck, sr)), FnTrig<0>::in_main(xb)};
-    fc = Fast{fma_(Ck, cr, -mul_(Sk, sr)), FnTrig<1>::in_main(xb)};
+    fs = Fast{flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k), FnTrig<0>::in_main(xb)};
+    fc = Fast{flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k), FnTrig<1>::in_main(xb)};
   }
   CR_F static bool is_big(float x) {
     uint32_t az = f2u(x) << 1;

@@ -220,6 +220,7 @@ def gen_trig():
     PI = mp.pi
     S = [mp.sin(j * PI / 16) for j in range(16)]
     arr("SIN16_HI", [dd(v)[0] for v in S]); arr("SIN16_LO", [dd(v)[1] for v in S])
+    arr("COS16_HI", [dd(mp.cos(j * PI / 16))[0] for j in range(16)])
     R = PI / 32 * mp.mpf("1.0005")
     gs = lambda s: (mp.sin(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else -mp.mpf(1) / 6
     cs, _ = chebfit(gs, mp.mpf(0), R ** 2, 2)
