@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kMaxDev = 16;
 constexpr size_t kChunk = size_t(1) << 22;  // host path pipeline chunk (elements)
+constexpr int kPipe = 4;                     // host path streams / staging sets
 
 FnEntry g_table[CRVEC_FN_COUNT];
 std::once_flag g_table_once;
@@ -42,9 +43,9 @@ struct Dev {
   int status = CRVEC_ENODEV;
   unsigned long long *counters = nullptr;  // [0] lanes (unused), [1] fast_undecided, [2] acc, [3] host
   // host-path staging
-  void *buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  void *buf[kPipe][3] = {};
   size_t buf_bytes = 0;
-  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaStream_t st[kPipe] = {};
 };
 Dev g_dev[kMaxDev];
 
@@ -126,9 +127,10 @@ int ensure_staging(Dev *D, size_t bytes) {
   return CRVEC_OK;
 }
 
-// Host-pointer path: chunks alternate between two streams so the H2D copy of
-// chunk i+1, the kernel of chunk i and the D2H copy of chunk i-1 overlap
-// (fully when the host buffers are pinned).
+// Host-pointer path: chunks rotate over kPipe streams (each with its own
+// staging buffers) so H2D copies, kernels and D2H copies of different chunks
+// overlap and both copy engines stay busy (fully when the host buffers are
+// pinned; with two streams an H2D would wait behind its stream's D2H).
 template <class T, class Launch>
 int host_pipeline(Dev *D, const T *x, T *y, T *y2, size_t n, Launch &&lf) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -138,7 +140,7 @@ int host_pipeline(Dev *D, const T *x, T *y, T *y2, size_t n, Launch &&lf) {
   size_t i = 0;
   for (size_t off = 0; off < n; off += chunk, ++i) {
     size_t cnt = n - off < chunk ? n - off : chunk;
-    int k = i & 1;
+    int k = (int)(i % kPipe);
     cudaStream_t s = D->st[k];
     T *dx = (T *)D->buf[k][0], *dy = (T *)D->buf[k][1], *dy2 = (T *)D->buf[k][2];
     cudaError_t e = cudaMemcpyAsync(dx, x + off, cnt * sizeof(T), cudaMemcpyHostToDevice, s);
