@@ -144,3 +144,42 @@ def test_accurate_path_self_check(cuda, name):
         total += n_acc
         assert (h == g[lo:lo + 8]).all(), f"{name}: forced-accurate chunk mismatch at {lo}"
     assert total > 1 << 20, total  # millions of lanes really went through the accurate path
+
+
+@pytest.mark.parametrize("name", crvec.F32_FUNCS)
+def test_inplace_vector_path_with_rare_lanes(cuda, oracle, name):
+    """Aligned in-place call large enough for the vector kernel (several grid
+    strides, ragged last step), inputs full of specials and hard lanes: the
+    rare path must resolve lanes before the in-place store overwrites them."""
+    n = (1 << 16) + 7
+    x = mixed_f32(name, n, seed=21)[:n]
+    for mode in (0, 3):
+        want = oracle.f32(crvec.ORACLE_NAME[name], x, mode)
+        v = cuda.from_numpy(x.view(np.float32).copy()).cuda()
+        crvec.eval_f32(name, v, mode, out=v)
+        ex, nbad = _mismatch_report(x, v.cpu().numpy().view(np.uint32), want)
+        assert nbad == 0, f"{name} mode {mode}: {ex}"
+
+
+@pytest.mark.parametrize("name", ["expf", "sinf", "sincosf"])
+def test_host_pipeline_multichunk(cuda, name):
+    """Host-pointer entry point over several 4M-element chunks rotating through
+    the staging streams equals the device entry point (validated above)."""
+    import ctypes
+    n = 3 * (1 << 22) + 5
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-80, 80, n).astype(np.float32)
+    L = crvec.lib()
+    fid = crvec.FN_IDS[name]
+    hy = np.empty(n, np.float32)
+    hy2 = np.empty(n, np.float32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    assert L.crvec_eval_f32(fid, p(x), p(hy), p(hy2) if name == "sincosf" else None, n, 1) == 0
+    xd = cuda.from_numpy(x).cuda()
+    yd = cuda.empty_like(xd)
+    yd2 = cuda.empty_like(xd)
+    s = ctypes.c_void_p(cuda.cuda.current_stream().cuda_stream)
+    assert L.crvec_eval_f32_dev(fid, xd.data_ptr(), yd.data_ptr(), yd2.data_ptr(), n, 1, s) == 0
+    assert (yd.cpu().numpy().view(np.uint32) == hy.view(np.uint32)).all()
+    if name == "sincosf":
+        assert (yd2.cpu().numpy().view(np.uint32) == hy2.view(np.uint32)).all()
