@@ -104,22 +104,17 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
                                                  RedTrig (&q)[NE], PHBlock &sh) {
   const int lane = threadIdx.x & 31;
   PHWarp &w = sh.warp[threadIdx.x >> 5];
-  // queue offsets: exclusive warp prefix sum of each lane's big-argument count
-  int nloc = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  // slot-major queue: one ballot per slot gives each big element its position
+  int pos[NE];
+  int total = 0;
 #pragma unroll
-  for (int e = 0; e < NE; ++e) nloc += big[e];
-  int incl = nloc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
+  for (int e = 0; e < NE; ++e) {
+    const unsigned b = __ballot_sync(kFull, big[e]);
+    pos[e] = total + __popc(b & lt);
+    total += __popc(b);
+    if (big[e]) w.qx[pos[e]] = (int)f2u(xs[e]);
   }
-  const int total = __shfl_sync(kFull, incl, 31);
-  const int base = incl - nloc;
-  int j = base;
-#pragma unroll
-  for (int e = 0; e < NE; ++e)
-    if (big[e]) w.qx[j++] = (int)f2u(xs[e]);
   __syncwarp();
   // all lanes reduce the compacted queue, 32 arguments per pass
   for (int b0 = 0; b0 < total; b0 += 32) {
@@ -131,13 +126,9 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
     }
   }
   __syncwarp();
-  j = base;
 #pragma unroll
   for (int e = 0; e < NE; ++e)
-    if (big[e]) {
-      q[e] = RedTrig{w.qx[j], w.rr[j]};
-      ++j;
-    }
+    if (big[e]) q[e] = RedTrig{w.qx[pos[e]], w.rr[pos[e]]};
   __syncwarp();
 }
 
