@@ -29,7 +29,7 @@ using namespace crvec;
 namespace {
 
 constexpr int kMaxDev = 16;
-constexpr size_t kChunk = size_t(1) << 22;  // host path pipeline chunk (elements)
+constexpr size_t kChunk = size_t(1) << 24;  // host path pipeline chunk (elements, measured: 2^21 10.3, 2^22 11.1, 2^24 11.4 Gelem/s)
 constexpr int kPipe = 4;                     // host path streams / staging sets
 
 FnEntry g_table[CRVEC_FN_COUNT];
