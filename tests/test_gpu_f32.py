@@ -163,10 +163,10 @@ def test_inplace_vector_path_with_rare_lanes(cuda, oracle, name):
 
 @pytest.mark.parametrize("name", ["expf", "sinf", "sincosf"])
 def test_host_pipeline_multichunk(cuda, name):
-    """Host-pointer entry point over several 4M-element chunks rotating through
+    """Host-pointer entry point over several staging chunks rotating through
     the staging streams equals the device entry point (validated above)."""
     import ctypes
-    n = 3 * (1 << 22) + 5
+    n = 2 * (1 << 24) + 5  # three 2^24-element chunks
     rng = np.random.default_rng(5)
     x = rng.uniform(-80, 80, n).astype(np.float32)
     L = crvec.lib()
