@@ -231,8 +231,8 @@ CR_F HypParts hyp_parts(double ax, double tab) {
   double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp), (kp >> 4) - 1);
   double Em = scale2(CR_TAB(tab, EXP2J_HI, km), (km >> 4) - 1);
   double s = mul_(q.r, q.r);
-  double sr = fma_(mul_(q.r, s), fma_(fma_(SINHQ[2], s, SINHQ[1]), s, SINHQ[0]), q.r);
-  double cr = fma_(s, fma_(fma_(COSHQ[2], s, COSHQ[1]), s, COSHQ[0]), 1.0);
+  double sr = fma_(mul_(q.r, s), fma_(SINHQ[1], s, SINHQ[0]), q.r);
+  double cr = fma_(s, fma_(COSHQ[1], s, COSHQ[0]), 1.0);
   return {sub_(Ep, Em), add_(Ep, Em), sr, cr};
 }
 struct HypDD {
@@ -260,7 +260,7 @@ CR_F HypDD hyp_parts_dd(double ax) {
 }
 
 struct FnSinh {
-  static constexpr uint32_t E = 128;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
@@ -286,7 +286,7 @@ struct FnSinh {
 };
 
 struct FnCosh {
-  static constexpr uint32_t E = 16;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
