@@ -24,8 +24,7 @@ CR_F double expq(double r) {
   return fma_(fma_(fma_(fma_(EXPQ[4], r, EXPQ[3]), r, EXPQ[2]), r, EXPQ[1]), r, EXPQ[0]);
 }
 CR_F double logq(double r) {
-  double q = fma_(LOGQ[6], r, LOGQ[5]);
-  q = fma_(q, r, LOGQ[4]);
+  double q = fma_(LOGQ[5], r, LOGQ[4]);
   q = fma_(q, r, LOGQ[3]);
   q = fma_(q, r, LOGQ[2]);
   q = fma_(q, r, LOGQ[1]);
@@ -367,7 +366,7 @@ CR_F RedLog red_log(double xd) {
 
 template <int BASE>  // 0: ln, 2: log2, 10: log10
 struct FnLogB {
-  static constexpr uint32_t E = 32;
+  static constexpr uint32_t E = 1024;
   struct Regs { int c; double l; };
   CR_F static void load(Regs &R) {
     R.c = CR_TAB_LOAD(LOG_C_HI);
@@ -420,7 +419,7 @@ using FnLog2 = FnLogB<2>;
 using FnLog10 = FnLogB<10>;
 
 struct FnLog1p {
-  static constexpr uint32_t E = 32;
+  static constexpr uint32_t E = 1024;
   struct Regs { int c; double l; };
   CR_F static void load(Regs &R) {
     R.c = CR_TAB_LOAD(LOG_C_HI);
