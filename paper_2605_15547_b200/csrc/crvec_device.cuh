@@ -111,7 +111,7 @@ CR_F double add_M(double a, double b) {
 CR_F double f2d(float f) { return (double)f; }
 CR_F double dabs(double a) { return std::fabs(a); }
 CR_F float fabs_(float a) { return std::fabs(a); }
-CR_F double rcp_approx(double x) { return (double)(float)(1.0 / x); }
+CR_F double rcp_approx(double x) { return (double)(float)(1.0 / x); }  // optimistic: MUFU.RCP64H is coarser
 CR_F double rsqrt_approx(double x) { return (double)(float)(1.0 / std::sqrt(x)); }
 CR_F float rcp_approx_f(float x) { return 1.0f / x; }
 CR_F double sqrt_rn(double x) { return std::sqrt(x); }
@@ -282,7 +282,9 @@ CR_F double sqrt_fast(double a) {
 CR_F double scale2(double a, int e) { return hilo2d(d2hi(a) + (e << 20), d2lo(a)); }
 
 // Division num/den to ~2^-52 relative: MUFU seed, one Newton step, one
-// residual correction (6 FP64 ops).
+// residual correction (6 FP64 ops). The residual step is required: a product
+// with the once-refined reciprocal alone fails the exhaustive tanf sweep
+// (MUFU.RCP64H seeds are too coarse for one Newton step).
 CR_F double div_fast(double num, double den) {
   double r = rcp_approx(den);
   double e = fma_(-den, r, 1.0);

@@ -310,7 +310,7 @@ struct FnCosh {
 struct FnTanh {
   // tanh|x| = E / (E + 2), E = expm1(2|x|) = T (1 + p) - 1 (T rounded: for
   // k = +-1 the cancellation costs ~2^-49.5, covered by E).
-  static constexpr uint32_t E = 128;
+  static constexpr uint32_t E = 512;
   struct Regs { double t; };
   CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
@@ -683,18 +683,6 @@ CR_F int atan_index_f(float yf, float xf) {
   return j < 0 ? 0 : (j > 15 ? 15 : j);
 }
 CR_F int atan_index(double Y, double X) { return atan_index_f((float)Y, (float)X); }
-CR_F double atan_t(double t) {
-  double s = mul_(t, t);
-  double q = fma_(fma_(fma_(ATANQ[3], s, ATANQ[2]), s, ATANQ[1]), s, ATANQ[0]);
-  return fma_(mul_(t, s), q, t);
-}
-CR_F double atan2_core(double Y, double X, double tab, int j) {
-  double S = CR_TAB(tab, SIN30_HI, j), C = CR_TAB(tab, SIN30_HI, 15 - j);
-  double num = fma_(Y, C, -mul_(X, S));
-  double den = fma_(X, C, mul_(Y, S));
-  double t = div_fast(num, den);
-  return fma_(i2d(j), PI_30_H, atan_t(t));
-}
 CR_F DD atan2_core_dd(DD Y, DD X) {
   int j = atan_index(Y.hi, X.hi);
   DD S = {SIN30_HI[j], SIN30_LO[j]}, C = {SIN30_HI[15 - j], SIN30_LO[15 - j]};
@@ -720,7 +708,7 @@ CR_F double atan_t2(double t) {
 }
 
 struct FnAtan {
-  static constexpr uint32_t E = 64;
+  static constexpr uint32_t E = 512;
   struct Regs { int a; double c, s; };
   CR_F static void load(Regs &R) {
     R.a = CR_TAB_LOAD(ATAN_A_HI);
