@@ -30,12 +30,13 @@ template <int FN>
 __device__ __forceinline__ void load_tables(F64Tab &T) {
   if (FN == 0) {
     for (int i = threadIdx.x; i < 64; i += kT64) {
-      T.ah[i] = EXP2D_A_HI[i]; T.al[i] = EXP2D_A_LO[i];
-      T.bh[i] = EXP2D_B_HI[i]; T.bl[i] = EXP2D_B_LO[i];
+      T.ta[i] = Pair64{EXP2D_A_HI[i], EXP2D_A_LO[i]};
+      T.tb[i] = Pair64{EXP2D_B_HI[i], EXP2D_B_LO[i]};
     }
   } else {
     for (int i = threadIdx.x; i < 512; i += kT64) {
-      T.lc[i] = LOGD5_C[i]; T.llh[i] = LOGD5_LT_HI[i]; T.lll[i] = LOGD5_LT_LO[i];
+      T.lc[i] = Pair64{LOGD5_C[i], LOGD5_LT_HI[i]};
+      T.lll[i] = LOGD5_LT_LO[i];
     }
   }
   __syncthreads();

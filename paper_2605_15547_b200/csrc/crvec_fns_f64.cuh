@@ -285,9 +285,14 @@ CR_F double logd_accurate(double x, int *undecided) {
 }
 
 // --------------------------------------------------------- fast paths ----
+// Shared-memory tables, laid out so each lookup is one 128-bit LDS.
+struct alignas(16) Pair64 {
+  double a, b;
+};
 struct F64Tab {
-  double ah[64], al[64], bh[64], bl[64];  // 2^(i/64), 2^(i/4096) as double-doubles
-  double lc[512], llh[512], lll[512];     // c_i (10 bits); -log(c_i): 2^-40 grid + rest
+  Pair64 ta[64], tb[64];  // (hi, lo) of 2^(i/64) and 2^(i/4096)
+  Pair64 lc[512];         // (c_i (10 bits), -log(c_i) on the 2^-40 grid)
+  double lll[512];        // -log(c_i) - the grid part
 };
 
 struct F64Out {
@@ -350,7 +355,8 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
     return {p, true};
   }
   // T = A B as an unnormalised DD (|Tl| < 2^-51 |Th|)
-  double ah = T.ah[ia], alo = T.al[ia], bh = T.bh[ib], blo = T.bl[ib];
+  const Pair64 A = T.ta[ia], B = T.tb[ib];
+  const double ah = A.a, alo = A.b, bh = B.a, blo = B.b;
   double Th = mul_(ah, bh);
   double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
   double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
@@ -385,7 +391,8 @@ CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
   int k = (int)d2lo(t);
   double R = fma_(kd, -0x1p-12, xs);  // exact, |R| <= 2^-13
   int N = k >> 12, ia = (k >> 6) & 63, ib = k & 63;
-  double ah = T.ah[ia], alo = T.al[ia], bh = T.bh[ib], blo = T.bl[ib];
+  const Pair64 A = T.ta[ia], B = T.tb[ib];
+  const double ah = A.a, alo = A.b, bh = B.a, blo = B.b;
   double Th = mul_(ah, bh);
   double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
   double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
@@ -408,7 +415,8 @@ CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   int e = (hh >> 20) + eadj;
   int i = (hh >> 11) & 511;
   double m = hilo2d(h - ((hh >> 20) << 20), d2lo(xs));
-  double r = fma_(m, T.lc[i], -1.0);               // exact
+  const Pair64 cl = T.lc[i];
+  double r = fma_(m, cl.a, -1.0);                  // exact
   DD s = two_prod(r, r);                          // r^2 exact
   const double *P = LOGD5_P;
   double p = fma_(fma_(fma_(fma_(fma_(fma_(P[6], r, P[5]), r, P[4]), r, P[3]), r, P[2]), r, P[1]), r, P[0]);
@@ -416,7 +424,7 @@ CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   DD a = fast_two_sum(r, -0.5 * s.hi);            // |r| > |r^2/2|
   // e ln2 + L: the high parts add exactly (both on the 2^-40 grid)
   double ed = i2d(e);
-  double th = fma_(ed, LN2_HD, T.llh[i]);
+  double th = fma_(ed, LN2_HD, cl.b);
   double tl = fma_(ed, LN2_LD, T.lll[i]);
   DD v = two_sum(th, a.hi);
   double lo = add_(add_(v.lo, tl), add_(fma_(-0.5, s.lo, a.lo), small));

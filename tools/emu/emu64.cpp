@@ -8,9 +8,12 @@ static F64Tab T;
 static void init() {
   static bool done = false;
   if (done) return;
-  std::memcpy(T.ah, EXP2D_A_HI, 512); std::memcpy(T.al, EXP2D_A_LO, 512);
-  std::memcpy(T.bh, EXP2D_B_HI, 512); std::memcpy(T.bl, EXP2D_B_LO, 512);
-  std::memcpy(T.lc, LOGD5_C, 4096); std::memcpy(T.llh, LOGD5_LT_HI, 4096); std::memcpy(T.lll, LOGD5_LT_LO, 4096);
+  for (int i = 0; i < 64; ++i) {
+    T.ta[i] = Pair64{EXP2D_A_HI[i], EXP2D_A_LO[i]};
+    T.tb[i] = Pair64{EXP2D_B_HI[i], EXP2D_B_LO[i]};
+  }
+  for (int i = 0; i < 512; ++i) T.lc[i] = Pair64{LOGD5_C[i], LOGD5_LT_HI[i]};
+  std::memcpy(T.lll, LOGD5_LT_LO, 4096);
   done = true;
 }
 template <int M>
