@@ -212,6 +212,27 @@ __device__ __forceinline__ void resolve_rare(const float (&xs)[NE], uint32_t (&y
   if (cnt) atomicAdd(counters, (unsigned long long)cnt);
 }
 
+// Rare path (store form, map kernels): runs after the vector stores; each
+// pass gathers every lane's lowest pending input from registers, resolves it
+// and overwrites the one output float with a scalar store (same thread,
+// program order), so no scatter back into the register results is needed.
+// In-place calls are safe: the inputs are still in registers.
+template <class F, int M, int NE, int VW>
+__device__ __forceinline__ void resolve_rare_store(const float (&xs)[NE], unsigned mask, float *yf,
+                                                   uint32_t fbase, unsigned long long *counters) {
+  int cnt = 0;
+  do {
+    const unsigned low = mask & (0u - mask);
+    const float xe = gather_slot<NE>(xs, low);
+    if (low) {
+      const int e = __ffs(mask) - 1;
+      yf[fbase + 32u * VW * (uint32_t)(e / VW) + (uint32_t)(e % VW)] = u2f(resolve_one<F, M>(xe, cnt));
+    }
+    mask &= ~low;
+  } while (__any_sync(kFull, mask != 0));
+  if (cnt) atomicAdd(counters, (unsigned long long)cnt);
+}
+
 template <class F, int M, int NE>
 __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)[NE],
                                            const typename F::Regs &R, PHBlock *sh,
@@ -240,6 +261,16 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw2.txt): float4s
 // per lane per step (nv) and the __launch_bounds__ min-blocks register cap
 // (minb; 256 threads per block).
+// Rare-path form per function (measured, profiles/r01/ab_rare_store.txt):
+// store form (resolve after the vector store, scalar overwrite) or register
+// form (gather + scatter before the store). The choice changes the main
+// path's register allocation, so it is taken per kernel.
+template <class F> struct RareStore { static constexpr bool value = false; };
+template <int B> struct RareStore<FnLogB<B>> { static constexpr bool value = true; };
+template <bool A> struct RareStore<FnAsinAcos<A>> { static constexpr bool value = true; };
+template <> struct RareStore<FnCosh> { static constexpr bool value = true; };
+template <> struct RareStore<FnTanh> { static constexpr bool value = true; };
+
 template <class F>
 struct KernelShape {
   static constexpr int vw = 4, nv = 2, minb = 3;
@@ -273,11 +304,23 @@ __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> 
     for (int j = 0; j < VW; ++j) xs[VW * k + j] = cur[k].v[j];
   }
   uint32_t ys[VW * NV];
-  eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
+  if constexpr (RareStore<F>::value) {
+    unsigned mask = fast_eval<F, M, VW * NV>(xs, ys, R, sh);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const uint32_t i = base + 32 * k;
-    if (i < nv) st_vec<VW>(y + i, ys + VW * k);
+    for (int k = 0; k < NV; ++k) {
+      const uint32_t i = base + 32 * k;
+      if (i < nv) st_vec<VW>(y + i, ys + VW * k);
+      else mask &= ~(((1u << VW) - 1u) << (VW * k));  // stale inputs past the end
+    }
+    if (__any_sync(kFull, mask != 0))
+      resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, VW * base, counters);
+  } else {
+    eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const uint32_t i = base + 32 * k;
+      if (i < nv) st_vec<VW>(y + i, ys + VW * k);
+    }
   }
 }
 
