@@ -261,7 +261,8 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw2.txt): float4s
 // per lane per step (nv) and the __launch_bounds__ min-blocks register cap
 // (minb; 256 threads per block).
-// Rare-path form per function (measured, profiles/r01/ab_rare_store.txt):
+// Rare-path form per function (measured, profiles/r01/ab_rare_store.txt,
+// profiles/r01/tune_store_form.txt):
 // store form (resolve after the vector store, scalar overwrite) or register
 // form (gather + scatter before the store). The choice changes the main
 // path's register allocation, so it is taken per kernel.
@@ -270,6 +271,7 @@ template <int B> struct RareStore<FnLogB<B>> { static constexpr bool value = tru
 template <bool A> struct RareStore<FnAsinAcos<A>> { static constexpr bool value = true; };
 template <> struct RareStore<FnCosh> { static constexpr bool value = true; };
 template <> struct RareStore<FnTanh> { static constexpr bool value = true; };
+template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = true; };
 
 template <class F>
 struct KernelShape {
@@ -285,6 +287,7 @@ template <> struct KernelShape<FnLog10> { static constexpr int vw = 4, nv = 2, m
 template <> struct KernelShape<FnAtan> { static constexpr int vw = 4, nv = 2, minb = 2; };
 template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 4, nv = 2, minb = 4; };
 template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
+template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 4, nv = 2, minb = 2; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step
 // into `nxt`, evaluate `cur`, store. Called alternately with the two register
