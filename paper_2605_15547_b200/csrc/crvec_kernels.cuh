@@ -384,10 +384,10 @@ __global__ void __launch_bounds__(kThreads) k_map_scalar(const float *x, float *
 // sincosf: one reduction, two outputs (1 in / 2 out = 12 B per element).
 // The rare mask carries the sin slots in bits 0..15 and the cos slots in
 // bits 16..31; one gather pass resolves either kind.
-template <int M, int NE>
-__device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s)[NE],
-                                             uint32_t (&c)[NE], const FnSin::Regs &R,
-                                             PHBlock *sh, unsigned long long *counters) {
+template <int M, int NE, bool STORE_FORM = false>
+__device__ __forceinline__ unsigned sincos_lanes(const float (&xs)[NE], uint32_t (&s)[NE],
+                                                 uint32_t (&c)[NE], const FnSin::Regs &R,
+                                                 PHBlock *sh, unsigned long long *counters) {
   static_assert(NE <= 16, "mask layout");
   RedTrig q[NE];
   bool big[NE];
@@ -409,6 +409,7 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
     mask |= (unsigned)((!a.main) | near_boundary(a.a, FnSin::E)) << e;
     mask |= (unsigned)((!b.main) | near_boundary(b.a, FnCos::E)) << (e + 16);
   }
+  if (STORE_FORM) return mask;
   if (__any_sync(kFull, mask != 0)) {
     int cnt = 0;
     do {
@@ -426,6 +427,34 @@ __device__ __forceinline__ void sincos_lanes(const float (&xs)[NE], uint32_t (&s
     } while (__any_sync(kFull, mask != 0));
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);
   }
+  return 0u;
+}
+
+#ifndef CRVEC_SINCOS_STORE
+#define CRVEC_SINCOS_STORE 1
+#endif
+constexpr bool kSincosStore = CRVEC_SINCOS_STORE;
+
+// Store form of the sincosf rare path (after both vector stores): scalar
+// overwrite of the one sin or cos output a pending bit names.
+template <int M, int NE>
+__device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigned mask, float *ys,
+                                                  float *yc, uint32_t fbase,
+                                                  unsigned long long *counters) {
+  int cnt = 0;
+  do {
+    const unsigned low = mask & (0u - mask);
+    const unsigned slot = (low | (low >> 16)) & 0xFFFFu;
+    const float xe = gather_slot<NE>(xs, slot);
+    if (low) {
+      const int e = (__ffs(low) - 1) & 15;
+      const uint32_t fi = fbase + 128u * (uint32_t)(e >> 2) + (uint32_t)(e & 3);
+      if (low >> 16) yc[fi] = u2f(resolve_one<FnCos, M>(xe, cnt));
+      else ys[fi] = u2f(resolve_one<FnSin, M>(xe, cnt));
+    }
+    mask &= ~low;
+  } while (__any_sync(kFull, mask != 0));
+  if (cnt) atomicAdd(counters, (unsigned long long)cnt);
 }
 
 template <int M, int NV>
@@ -445,18 +474,22 @@ __device__ __forceinline__ void sincos_step(const float4 *__restrict__ x, float4
     xs[4 * k + 3] = cur[k].w;
   }
   uint32_t s[4 * NV], c[4 * NV];
-  sincos_lanes<M, 4 * NV>(xs, s, c, R, sh, counters);
+  unsigned mask = sincos_lanes<M, 4 * NV, kSincosStore>(xs, s, c, R, sh, counters);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = base + 32 * k;
     if (i < n4) {
       st_stream(ys + i, make_float4(u2f(s[4 * k]), u2f(s[4 * k + 1]), u2f(s[4 * k + 2]), u2f(s[4 * k + 3])));
       st_stream(yc + i, make_float4(u2f(c[4 * k]), u2f(c[4 * k + 1]), u2f(c[4 * k + 2]), u2f(c[4 * k + 3])));
+    } else {
+      mask &= ~((15u << (4 * k)) | (15u << (4 * k + 16)));  // stale inputs past the end
     }
   }
+  if (kSincosStore && __any_sync(kFull, mask != 0))
+    sincos_rare_store<M, 4 * NV>(xs, mask, (float *)ys, (float *)yc, 4u * base, counters);
 }
 
-constexpr int kSincosNV = 2, kSincosMinB = 3;
+constexpr int kSincosNV = 2, kSincosMinB = 2;
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, kSincosMinB)
