@@ -262,14 +262,15 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // per lane per step (nv) and the __launch_bounds__ min-blocks register cap
 // (minb; 256 threads per block).
 // Rare-path form per function (measured, profiles/r01/ab_rare_store.txt,
-// profiles/r01/tune_store_form.txt):
+// profiles/r01/tune_store_form.txt, profiles/r01/tune_vw8.txt):
 // store form (resolve after the vector store, scalar overwrite) or register
 // form (gather + scatter before the store). The choice changes the main
 // path's register allocation, so it is taken per kernel.
 template <class F> struct RareStore { static constexpr bool value = false; };
 template <int B> struct RareStore<FnLogB<B>> { static constexpr bool value = true; };
 template <bool A> struct RareStore<FnAsinAcos<A>> { static constexpr bool value = true; };
-template <> struct RareStore<FnCosh> { static constexpr bool value = true; };
+template <> struct RareStore<FnExpm1> { static constexpr bool value = true; };
+template <> struct RareStore<FnRsqrt> { static constexpr bool value = true; };
 template <> struct RareStore<FnTanh> { static constexpr bool value = true; };
 template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = true; };
 
@@ -279,13 +280,16 @@ struct KernelShape {
 };
 template <> struct KernelShape<FnExp2> { static constexpr int vw = 4, nv = 4, minb = 2; };
 template <> struct KernelShape<FnExp10> { static constexpr int vw = 4, nv = 4, minb = 2; };
-template <> struct KernelShape<FnExp> { static constexpr int vw = 4, nv = 2, minb = 4; };
-template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 4; };
+template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnLog10> { static constexpr int vw = 4, nv = 2, minb = 4; };
 template <> struct KernelShape<FnAtan> { static constexpr int vw = 4, nv = 2, minb = 2; };
-template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
 template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 4, nv = 2, minb = 2; };
 
@@ -771,20 +775,29 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
   constexpr int VW = KernelShape<F>::vw, NV = KernelShape<F>::nv;
   static int mb_vec = max_blocks(k_map_vec<F, M>);
   static int mb_sc = max_blocks(k_map_scalar<F, M>);
-  bool aligned = (((uintptr_t)x | (uintptr_t)y) & (4 * VW - 1)) == 0;
-  uint64_t nvec = aligned ? n / VW : 0;
+  constexpr uintptr_t A = 4 * VW - 1;  // vector alignment mask (16 or 32 bytes)
+  auto scalar = [&](const float *xx, float *yy, uint64_t m) {
+    if (m) k_map_scalar<F, M><<<grid_for((m + 31) / 32, mb_sc), kThreads, 0, s>>>(xx, yy, m, ctr);
+  };
+  // x and y misaligned by the same amount: peel a scalar head up to the
+  // vector boundary (a relative misalignment leaves only the element kernel)
+  uint64_t head = 0;
+  if ((((uintptr_t)x ^ (uintptr_t)y) & A) == 0 && ((uintptr_t)x & 3) == 0 && ((uintptr_t)x & A))
+    head = ((A + 1 - ((uintptr_t)x & A)) & A) / 4;
+  if (head > n) head = n;
+  const bool aligned = ((((uintptr_t)(x + head)) | ((uintptr_t)(y + head))) & A) == 0;
+  const uint64_t nvec = aligned ? (n - head) / VW : 0;
+  scalar(x, y, aligned ? head : 0);
+  const float *xv = aligned ? x + head : x;
+  float *yv = aligned ? y + head : y;
   // the kernel indexes vectors with 32 bits: launches of at most 2^31 vectors
   constexpr uint64_t kMaxNV = uint64_t(1) << 31;
   for (uint64_t off = 0; off < nvec; off += kMaxNV) {
     uint64_t m = nvec - off < kMaxNV ? nvec - off : kMaxNV;
     const unsigned g = grid_for((m + 32 * NV - 1) / (32 * NV), mb_vec);
-    k_map_vec<F, M><<<g, kThreads, 0, s>>>(x + VW * off, y + VW * off, (uint32_t)m, ctr);
+    k_map_vec<F, M><<<g, kThreads, 0, s>>>(xv + VW * off, yv + VW * off, (uint32_t)m, ctr);
   }
-  uint64_t rem = n - VW * nvec;
-  if (rem) {
-    k_map_scalar<F, M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(x + VW * nvec, y + VW * nvec,
-                                                                            rem, ctr);
-  }
+  scalar(xv + VW * nvec, yv + VW * nvec, (uint64_t)((x + n) - (xv + VW * nvec)));
   return cudaGetLastError();
 }
 

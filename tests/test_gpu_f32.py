@@ -183,3 +183,20 @@ def test_host_pipeline_multichunk(cuda, name):
     assert (yd.cpu().numpy().view(np.uint32) == hy.view(np.uint32)).all()
     if name == "sincosf":
         assert (yd2.cpu().numpy().view(np.uint32) == hy2.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("name", ["logf", "expf", "sinf"])
+@pytest.mark.parametrize("ox,oy", [(4, 4), (1, 1), (4, 0), (0, 3)])
+def test_offset_pointers_head_peel(cuda, oracle, name, ox, oy):
+    """Device pointers offset by ox / oy floats from a 256-byte boundary: equal
+    offsets peel a scalar head up to the 128/256-bit vector boundary, unequal
+    ones take the element kernel; results are identical either way."""
+    n = (1 << 18) + 3
+    x = mixed_f32(name, n, seed=31 + ox)[:n]
+    want = oracle.f32(crvec.ORACLE_NAME[name], x, 0)
+    bx = cuda.zeros(n + 8, dtype=cuda.float32, device="cuda")
+    by = cuda.zeros(n + 8, dtype=cuda.float32, device="cuda")
+    bx[ox:ox + n] = cuda.from_numpy(x.view(np.float32)).cuda()
+    crvec.eval_f32(name, bx[ox:ox + n], 0, out=by[oy:oy + n])
+    ex, nbad = _mismatch_report(x, by[oy:oy + n].cpu().numpy().view(np.uint32), want)
+    assert nbad == 0, f"{name} ({ox},{oy}): {ex}"
