@@ -481,13 +481,14 @@ struct RedTrig {
 CR_F RedTrig red_trig_small(double xd) {
   double t = fma_(xd, INV_PI_16, SHIFTER);
   double kd = sub_(t, SHIFTER);
-  double r = fma_(kd, -PI_16_H, xd);
-  r = fma_(kd, -PI_16_M, r);
-  r = fma_(kd, -PI_16_L, r);
+  // two-part Cody-Waite, valid for |x| < 2^12 (larger |x| take Payne-Hanek):
+  // k * PI_16_A is exact (36-bit constant), the tail error is < 2^-76
+  double r = fma_(kd, -PI_16_A, xd);
+  r = fma_(kd, -PI_16_B, r);
   return {(int)d2lo(t), r};
 }
 
-// Payne-Hanek for |x| >= 2^17 (binary32 x = M * 2^(ex-23)):
+// Payne-Hanek for |x| >= 2^12 (binary32 x = M * 2^(ex-23)):
 // x*16/pi mod 32 from a 32*NW-bit window of 1/pi times the 24-bit M.
 // Returns k mod 32 (of |x|) and the 64-bit signed fraction (units 2^-64),
 // plus the next 64 (NW >= 5) or 59 (NW = 4) fraction bits.
@@ -631,7 +632,7 @@ struct FnTrig {
   }
   CR_F static bool is_big(float x) {
     uint32_t az = f2u(x) << 1;
-    return az >= (0x48000000u << 1) && az < 0xFF000000u;  // 2^17 <= |x| < inf
+    return az >= (0x45800000u << 1) && az < 0xFF000000u;  // 2^12 <= |x| < inf
   }
   template <int M>
   CR_F static uint32_t special(float x) {

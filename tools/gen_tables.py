@@ -238,6 +238,9 @@ def gen_trig():
     scalar("INV_PI_16", d(16 / PI))
     h, m, l = split3(PI / 16, 33, 33)
     scalar("PI_16_H", h); scalar("PI_16_M", m); scalar("PI_16_L", l)
+    # two-part split for |x| < 2^12 (k < 2^14.4: k * PI_16_A exact with 36 bits)
+    a = trunc_bits(PI / 16, 36)
+    scalar("PI_16_A", a); scalar("PI_16_B", d(PI / 16 - a))
     # four-part split for the DD slow path
     p1, p2, rest = split3(PI / 16, 33, 33)
     p3 = trunc_bits(PI / 16 - p1 - p2, 33)
