@@ -87,9 +87,10 @@ __device__ __noinline__ DD slow_dd(float x) {
 
 // ---------------------------------------------- warp-cooperative Payne-Hanek
 // Per-warp staging: the big-argument elements of the warp's 32 x NE slots are
-// compacted (warp prefix sum of per-lane counts) into a queue, reduced 32 at
-// a time by all lanes, and read back by their owners. One pass serves up to 32 big arguments however
-// they are spread over lanes and slots.
+// compacted (one ballot per slot: slot-major queue positions) into a shared
+// queue, reduced 32 at a time by all lanes, and read back by their owners.
+// One pass serves up to 32 big arguments however they are spread over lanes
+// and slots.
 struct PHWarp {
   double rr[256];
   int qx[256];  // queued x bits, overwritten by the reduced k
@@ -241,7 +242,7 @@ __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)
   if (__any_sync(kFull, mask != 0)) resolve_rare<F, M, NE>(xs, ys, mask, counters);
 }
 
-// Shared staging exists only in the trig kernels (34 KB per block).
+// Shared staging exists only in the trig kernels (24 KB per block).
 template <class F>
 __device__ __forceinline__ PHBlock *ph_storage() {
   if constexpr (IsTrig<F>::value) {
@@ -255,12 +256,13 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 }
 
 // ------------------------------------------------------------ map kernels ----
-// 4 elements (one float4) per lane per iteration; the loop trip count is
-// warp-uniform so the register-table shuffles always see a full warp.
+// NV vectors of VW floats per lane per step; the loop trip count is warp-
+// uniform so the register-table shuffles always see a full warp.
 // Kernel shape per function, chosen by measurement (tools/gpu_ab2.sh over
-// tools/mk_shape_variants.sh builds; profiles/r01/shapes_sw2.txt): float4s
-// per lane per step (nv) and the __launch_bounds__ min-blocks register cap
-// (minb; 256 threads per block).
+// tools/mk_shape_variants.sh / mk_tune_variants.sh builds;
+// profiles/r01/shapes_sw2.txt, tune_*.txt): vector width (vw 4: 128-bit,
+// vw 8: 256-bit accesses), vectors per lane per step (nv) and the
+// __launch_bounds__ min-blocks register cap (minb; 256 threads per block).
 // Rare-path form per function (measured, profiles/r01/ab_rare_store.txt,
 // profiles/r01/tune_store_form.txt, profiles/r01/tune_vw8.txt):
 // store form (resolve after the vector store, scalar overwrite) or register
