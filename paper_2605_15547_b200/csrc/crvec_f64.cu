@@ -89,8 +89,7 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t in = base + stride + 32 * k;
-    if (2ull * in + 1 < n) nxt[k] = __ldcs(x2 + in);
-    else if (2ull * in < n) nxt[k].x = x[2ull * in];  // odd n: last slot holds one double
+    if (in < n2) nxt[k] = __ldcs(x2 + in);  // n is even: every slot holds two doubles
   }
   double xv[2 * NV];
   F64Out r[2 * NV];
@@ -106,14 +105,11 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = base + 32 * k;
-    const uint64_t i0 = 2ull * i;
-    if (i0 + 1 < n) {
+    if (i < n2) {
       __stcs(y2 + i, make_double2(r[2 * k].y, r[2 * k + 1].y));
-    } else if (i0 < n) {
-      y[i0] = r[2 * k].y;
+      und |= (unsigned)(!r[2 * k].decided) << (2 * k);
+      und |= (unsigned)(!r[2 * k + 1].decided) << (2 * k + 1);
     }
-    und |= (unsigned)(i0 < n && !r[2 * k].decided) << (2 * k);
-    und |= (unsigned)(i0 + 1 < n && !r[2 * k + 1].decided) << (2 * k + 1);
   }
   // compact undecided lanes into the warp's side queue
   if (__any_sync(0xffffffffu, und != 0)) {
@@ -147,7 +143,7 @@ __global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *
   F64Queue &q = Q[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   int qn = 0;  // warp-uniform queue length
-  // 16-byte aligned x / y (the launcher guarantees it; odd n handled per lane)
+  // 16-byte aligned x / y and an even n (the launcher guarantees both)
   const double2 *x2 = reinterpret_cast<const double2 *>(x);
   double2 *y2 = reinterpret_cast<double2 *>(y);
   const uint32_t n2 = (uint32_t)((n + 1) / 2);
@@ -159,8 +155,7 @@ __global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *
     va[k] = make_double2(1.0, 1.0);
     vb[k] = va[k];
     const uint32_t i = base + 32 * k;
-    if (2ull * i + 1 < n) va[k] = __ldcs(x2 + i);
-    else if (2ull * i < n) va[k].x = x[2ull * i];
+    if (i < n2) va[k] = __ldcs(x2 + i);
   }
   while (base - lane < n2) {
     f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, ctr);
@@ -214,8 +209,10 @@ cudaError_t launch64(const double *x, double *y, uint64_t n, cudaStream_t s,
   if (head) k_f64_scalar<FN, M><<<1, kT64, 0, s>>>(x, y, 1, ctr);
   // 32-bit double2 slot indices: launches of at most 2^32 doubles
   constexpr uint64_t kMax = uint64_t(1) << 32;
-  for (uint64_t off = head; off < n; off += kMax) {
-    const uint64_t m = n - off < kMax ? n - off : kMax;
+  const uint64_t body = (n - head) & ~uint64_t(1);  // even count for the double2 kernel
+  if (head + body < n) k_f64_scalar<FN, M><<<1, kT64, 0, s>>>(x + n - 1, y + n - 1, 1, ctr);
+  for (uint64_t off = head; off < head + body; off += kMax) {
+    const uint64_t m = head + body - off < kMax ? head + body - off : kMax;
     constexpr int NV = F64Shape<FN>::nv;
     uint64_t blocks = ((m + 1) / 2 + kT64 * NV - 1) / (kT64 * NV);
     if (blocks > F64Shape<FN>::waves * (uint64_t)maxb) blocks = F64Shape<FN>::waves * (uint64_t)maxb;
