@@ -64,7 +64,8 @@ def trig_input(n: int, seed: int = 4) -> np.ndarray:
     return np.where(rng.integers(0, 8, n) == 0, big, x)
 
 
-def device_input(name: str, n: int, dist: str = "config", seed: int = 7, device: str = "cuda"):
+def device_input(name: str, n: int, dist: str = "config", seed: int = 7, device: str = "cuda",
+                 specials: bool = True):
     """The same distributions as above generated on the device with torch (for
     the perf tools: 2^28-element inputs in milliseconds; not bit-identical to
     the numpy generators). Returns a float32 tensor."""
@@ -92,10 +93,11 @@ def device_input(name: str, n: int, dist: str = "config", seed: int = 7, device:
         x = ubits(n, 0x7F800000)
         k = torch.randint(0, 1000, (n,), generator=g, device=device)
         x = torch.where(k < 10, ubits(n, 0x00800000 - 1) + 1, x)
-        for kk, v in ((10, 0), (11, 0x80000000), (12, 0x7F800000), (13, 0xFF800000),
-                      (14, 0x7FC12345), (15, 0xFFA54321)):
-            x = torch.where(k == kk, torch.full_like(x, v), x)
-        x = torch.where(k == 16, x | 0x80000000, x)
+        if specials:
+            for kk, v in ((10, 0), (11, 0x80000000), (12, 0x7F800000), (13, 0xFF800000),
+                          (14, 0x7FC12345), (15, 0xFFA54321)):
+                x = torch.where(k == kk, torch.full_like(x, v), x)
+            x = torch.where(k == 16, x | 0x80000000, x)
         if name == "log1pf":
             u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
             neg = (-u).to(torch.float32).view(torch.int32).to(torch.int64) & 0xFFFFFFFF

@@ -36,7 +36,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--fn", nargs="*")
     ap.add_argument("--mode", type=int, default=0)
-    ap.add_argument("--dist", default="config", choices=["config", "uniform"])
+    ap.add_argument("--dist", default="config", choices=["config", "uniform", "nospecial"])
     ap.add_argument("--no-f64", action="store_true")
     a = ap.parse_args()
     n = 1 << a.n
@@ -52,7 +52,8 @@ def main():
     y2 = torch.empty(n, dtype=torch.float32, device="cuda")
     rows = []
     for name in names:
-        x = device_input(name, n, a.dist)
+        x = device_input(name, n, "config" if a.dist == "nospecial" else a.dist,
+                         specials=a.dist != "nospecial")
         fid = crvec.FN_IDS[name]
         for _ in range(3):
             L.crvec_eval_f32_dev(fid, x.data_ptr(), y.data_ptr(), y2.data_ptr(), n, a.mode, sp)
