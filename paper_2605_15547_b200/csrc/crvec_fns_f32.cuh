@@ -389,13 +389,13 @@ struct FnLogB {
     return Fast{a, in_main(xb)};
   }
   CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < +Inf
+  // branch-free: +-0 -> -Inf, +Inf -> +Inf, NaN -> quiet(x), x < 0 -> qNaN
   template <int M>
   CR_F static uint32_t special(float x) {
-    uint32_t xb = f2u(x);
-    if (nan_bits(xb)) return quiet_bits(xb);
-    if ((xb << 1) == 0) return 0xFF800000u;
-    if (xb == 0x7F800000u) return 0x7F800000u;
-    return 0x7FC00000u;  // x < 0
+    const uint32_t xb = f2u(x);
+    uint32_t r = (xb << 1) == 0 ? 0xFF800000u : 0x7FC00000u;
+    r = xb == 0x7F800000u ? 0x7F800000u : r;
+    return nan_bits(xb) ? quiet_bits(xb) : r;
   }
   CR_F static DD log_dd_core(int e, int i, DD r) {
     // log1p(r) = sum_{n=1}^{24} (-1)^(n+1) r^n / n

@@ -226,8 +226,10 @@ __device__ __forceinline__ void resolve_rare_store(const float (&xs)[NE], unsign
     const unsigned low = mask & (0u - mask);
     const float xe = gather_slot<NE>(xs, low);
     if (low) {
-      const int e = __ffs(mask) - 1;
-      yf[fbase + 32u * VW * (uint32_t)(e / VW) + (uint32_t)(e % VW)] = u2f(resolve_one<F, M>(xe, cnt));
+      static_assert((NE & (NE - 1)) == 0, "NE: power of two");
+      // unsigned and bounded (mask has NE bits): / and % fold to shifts and masks
+      const uint32_t e = ((uint32_t)__ffs(mask) - 1u) & (NE - 1u);
+      yf[fbase + 32u * VW * (e / VW) + (e % VW)] = u2f(resolve_one<F, M>(xe, cnt));
     }
     mask &= ~low;
   } while (__any_sync(kFull, mask != 0));
@@ -453,8 +455,8 @@ __device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigne
     const unsigned slot = (low | (low >> 16)) & 0xFFFFu;
     const float xe = gather_slot<NE>(xs, slot);
     if (low) {
-      const int e = (__ffs(low) - 1) & 15;
-      const uint32_t fi = fbase + 128u * (uint32_t)(e >> 2) + (uint32_t)(e & 3);
+      const uint32_t e = ((uint32_t)__ffs(low) - 1u) & 15u;
+      const uint32_t fi = fbase + 128u * (e >> 2) + (e & 3u);
       if (low >> 16) yc[fi] = u2f(resolve_one<FnCos, M>(xe, cnt));
       else ys[fi] = u2f(resolve_one<FnSin, M>(xe, cnt));
     }
