@@ -230,17 +230,31 @@ def run_sweep(rank, world, fns):
     return secs, mism, checked
 
 
+def _libm_ops():
+    import torch
+    return {"expf": torch.exp, "exp2f": torch.exp2, "expm1f": torch.expm1, "logf": torch.log,
+            "log2f": torch.log2, "log10f": torch.log10, "log1pf": torch.log1p, "sinf": torch.sin,
+            "cosf": torch.cos, "tanf": torch.tan, "asinf": torch.asin, "acosf": torch.acos,
+            "atanf": torch.atan, "sinhf": torch.sinh, "coshf": torch.cosh, "tanhf": torch.tanh,
+            "rsqrtf": torch.rsqrt}
+
+
+LIBM_OPS = {}
+
+
 def all_functions_table(n=1 << 28, reps=5):
     """Device throughput of every binary32 function (and the binary64 pair) at
     2^28 (2^26 for binary64), inputs generated on the device: the configs'
     distributions for the log and trig families, uniform over each function's
-    interesting range otherwise. Median of `reps` event-timed launches."""
+    interesting range otherwise. Median of `reps` event-timed launches; next to
+    it, PyTorch's non-CR CUDA libm kernel on the same array (the cost of CR)."""
     import ctypes
     import torch
     import paper_2605_15547_b200 as crvec
-    from tests.inputs import RANGES
+    from tests.inputs import device_input
     peak, _ = peaks()
     L = crvec.lib()
+    LIBM_OPS.update(_libm_ops())
     s = torch.cuda.current_stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     g = torch.Generator(device="cuda")
@@ -263,19 +277,19 @@ def all_functions_table(n=1 << 28, reps=5):
         return float(np.median(ts))
 
     for name in crvec.F32_FUNCS + ["sincosf"]:
-        lo, hi = RANGES[name]
-        x = torch.rand(n, device="cuda", generator=g, dtype=torch.float32) * (hi - lo) + lo
-        if name in ("sinf", "cosf", "tanf", "sincosf"):  # config C3: 1/8 large-argument tail
-            big = torch.randint(0, 8, (n,), device="cuda", generator=g) == 0
-            e = torch.randint(142, 255, (n,), device="cuda", generator=g, dtype=torch.int32)
-            m = torch.randint(0, 1 << 23, (n,), device="cuda", generator=g, dtype=torch.int32)
-            sgn = torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int32) << 31
-            xb = (sgn | (e << 23) | m).view(torch.float32)
-            x = torch.where(big, xb, x)
+        # config C2 (log family: specials injected) / C3 (trig: 1/8 large-argument
+        # tail) distributions, uniform over the function's range otherwise
+        x = device_input(name, n, "config")
         fid = crvec.FN_IDS[name]
         t = timed(lambda: L.crvec_eval_f32_dev(fid, x.data_ptr(), y.data_ptr(), y2.data_ptr(), n, 0, sp))
         bpe = 12 if name == "sincosf" else 8
         out[name] = {"gelem_s": round(n / t / 1e9, 1), "frac_hbm": round(bpe * n / t / 1e9 / peak, 3)}
+        # the paper's Table III analogue: the same array through PyTorch's
+        # (non-CR, ~1-ulp CUDA libm) elementwise kernel, for the cost of CR
+        op = LIBM_OPS.get(name)
+        if op is not None:
+            tl = timed(lambda: op(x, out=y))
+            out[name]["torch_libm_gelem_s"] = round(n / tl / 1e9, 1)
         del x
     n64 = 1 << 26
     for name, lo, hi in (("exp2", -20.0, 20.0), ("log", 0.125, 8.0)):
