@@ -434,12 +434,21 @@ struct FnLog1p {
     double r = fma_(q.m, c, -1.0);
     double p = fma_(mul_(r, r), logq(r), r);
     double a = add_(fma_(i2d(q.e), LN2_D, L), p);
-    // |x| <= 2^-26 is ~40% of all bit patterns: keep its rule on the main
-    // path (x - x^2/2 lies just below x; the value is far from boundaries).
-    double xd = f2d(x);
-    if ((xb << 1) <= 0x65000000u) a = fma_(-dabs(xd), 0x1p-36, xd);
-    // main: 0 < |x| < inf and x > -1
+    // main: 0 < |x| < inf and x > -1. Tiny |x| (the kernels apply tiny_bits)
     return Fast{a, in_main(xb)};
+  }
+  // |x| <= 2^-26 is ~40% of all bit patterns (79% of the config-2 mix): its
+  // rule stays on the main path, applied to the result bits after the
+  // conversion. log1p(x) = x - x^2/2 + ... lies strictly below x and within
+  // x^2/2 < 2^-27 |x| of it, so in mode M it rounds to x (RNE, RU), to the
+  // float below x (RD), or toward zero from there (RZ): an integer +-1.
+  static constexpr bool kTinyRule = true;
+  CR_F static bool is_tiny(uint32_t xb) { return (xb << 1) <= 0x65000000u; }
+  template <int M>
+  CR_F static uint32_t tiny_bits(uint32_t xb) {
+    if (M == RNE || M == RU) return xb;
+    if (M == RZ) return (int)xb < 0 ? xb : xb - 1u;  // positive: the float below x
+    return (int)xb < 0 ? xb + 1u : xb - 1u;          // RD: next float toward -Inf
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 2u, 0xFF000000u) && xb < 0xBF800000u; }
   template <int M>

@@ -156,6 +156,11 @@ __device__ __forceinline__ void fast_lanes(const float (&xs)[NE], Fast (&f)[NE],
   }
 }
 
+template <class F, class = void>
+struct HasTinyRule { static constexpr bool value = false; };
+template <class F>
+struct HasTinyRule<F, decltype((void)F::kTinyRule)> { static constexpr bool value = F::kTinyRule; };
+
 // Common path for NE elements per lane: fast approximation, one static-mode
 // conversion, and the per-lane mask of rare slots (bit e: slot e is outside
 // the main range, or undecided by the rounding test).
@@ -169,7 +174,14 @@ __device__ __forceinline__ unsigned fast_eval(const float (&xs)[NE], uint32_t (&
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     ys[e] = f2u(cvt_f32<M>(f[e].a));
-    mask |= (unsigned)((!f[e].main) | near_boundary(f[e].a, F::E)) << e;
+    bool rare = (!f[e].main) | near_boundary(f[e].a, F::E);
+    if constexpr (HasTinyRule<F>::value) {  // log1pf: tiny-argument rule on the result bits
+      const uint32_t xb = f2u(xs[e]);
+      const bool tiny = F::is_tiny(xb);
+      ys[e] = tiny ? F::template tiny_bits<M>(xb) : ys[e];
+      rare = rare & !(tiny & f[e].main);
+    }
+    mask |= (unsigned)rare << e;
   }
   return mask;
 }
@@ -287,7 +299,7 @@ template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, m
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 2, minb = 2; };
-template <> struct KernelShape<FnLog1p> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 1, minb = 3; };
@@ -560,6 +572,17 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 template <class F>
 __device__ __forceinline__ void finish4(float x, Fast f, uint32_t (&y)[4], bool &fail) {
+  if constexpr (HasTinyRule<F>::value) {
+    const uint32_t xb = f2u(x);
+    if (f.main && F::is_tiny(xb)) {  // the map kernels' result-bits rule
+      fail = false;
+      y[0] = F::template tiny_bits<RNE>(xb);
+      y[1] = F::template tiny_bits<RZ>(xb);
+      y[2] = F::template tiny_bits<RU>(xb);
+      y[3] = F::template tiny_bits<RD>(xb);
+      return;
+    }
+  }
   if (f.main) {
     y[0] = finish<RNE>(f, fail, F::E);
     bool d;
