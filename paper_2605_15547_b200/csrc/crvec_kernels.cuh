@@ -450,10 +450,8 @@ __device__ __forceinline__ unsigned sincos_lanes(const float (&xs)[NE], uint32_t
   return 0u;
 }
 
-#ifndef CRVEC_SINCOS_STORE
-#define CRVEC_SINCOS_STORE 1
-#endif
-constexpr bool kSincosStore = CRVEC_SINCOS_STORE;
+// sincosf takes the store form of the rare path (measured, profiles/r01/ab_rare_store.txt)
+constexpr bool kSincosStore = true;
 
 // Store form of the sincosf rare path (after both vector stores): scalar
 // overwrite of the one sin or cos output a pending bit names.
