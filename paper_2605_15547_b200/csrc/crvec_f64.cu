@@ -15,8 +15,12 @@ constexpr int kW64 = kT64 / 32;
 // Kernel shape per function (measured, profiles/r01/f64_shapes.txt): double2
 // per lane per step, __launch_bounds__ min blocks per SM, grid waves.
 template <int FN> struct F64Shape;
-template <> struct F64Shape<0> { static constexpr int nv = 1, minb = 4, waves = 4; };  // exp2
-template <> struct F64Shape<1> { static constexpr int nv = 2, minb = 3, waves = 1; };  // log
+// dist = prefetch distance in loop steps; measured per function (profiles/r01/f64_shapes.txt)
+#ifndef CRVEC_LOG64_SHAPE
+#define CRVEC_LOG64_SHAPE nv = 2, minb = 3, waves = 1, dist = 1
+#endif
+template <> struct F64Shape<0> { static constexpr int nv = 1, minb = 4, waves = 4, dist = 2; };  // exp2
+template <> struct F64Shape<1> { static constexpr int CRVEC_LOG64_SHAPE; };                      // log
 constexpr int kF64MaxNV = 2;
 constexpr int kQ = 32 + 32 * 2 * kF64MaxNV;  // per-warp queue capacity: < 32 left + one step
 
@@ -88,7 +92,7 @@ __device__ __forceinline__ void f64_step(const double2 *__restrict__ x2, double2
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const uint32_t in = base + stride + 32 * k;
+    const uint32_t in = base + F64Shape<FN>::dist * stride + 32 * k;
     if (in < n2) nxt[k] = __ldcs(x2 + in);  // n is even: every slot holds two doubles
   }
   double xv[2 * NV];
@@ -149,20 +153,37 @@ __global__ void __launch_bounds__(kT64, F64Shape<FN>::minb) k_f64(const double *
   const uint32_t n2 = (uint32_t)((n + 1) / 2);
   const uint32_t stride = gridDim.x * (uint32_t)(kT64 * NV);
   uint32_t base = ((blockIdx.x * kT64 + threadIdx.x) >> 5) * (32 * NV) + lane;
-  double2 va[NV], vb[NV];
+  double2 va[NV], vb[NV], vc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     va[k] = make_double2(1.0, 1.0);
     vb[k] = va[k];
+    vc[k] = va[k];
     const uint32_t i = base + 32 * k;
     if (i < n2) va[k] = __ldcs(x2 + i);
+    if (F64Shape<FN>::dist == 2 && i + stride < n2) vb[k] = __ldcs(x2 + i + stride);
   }
-  while (base - lane < n2) {
-    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, ctr);
-    base += stride;
-    if (base - lane >= n2) break;
-    f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, ctr);
-    base += stride;
+  if constexpr (F64Shape<FN>::dist == 2) {
+    // three register buffers rotated: loads run two steps ahead (the binary64
+    // kernels stream 16 B per element and are memory-latency bound)
+    while (base - lane < n2) {
+      f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vc, T, q, qn, ctr);
+      base += stride;
+      if (base - lane >= n2) break;
+      f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, ctr);
+      base += stride;
+      if (base - lane >= n2) break;
+      f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vc, vb, T, q, qn, ctr);
+      base += stride;
+    }
+  } else {
+    while (base - lane < n2) {
+      f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, va, vb, T, q, qn, ctr);
+      base += stride;
+      if (base - lane >= n2) break;
+      f64_step<FN, M, NV>(x2, y2, x, y, n2, n, base, stride, vb, va, T, q, qn, ctr);
+      base += stride;
+    }
   }
   __syncwarp();
   if (qn) drain<FN, M>(q, 0, qn, T, y, ctr);
