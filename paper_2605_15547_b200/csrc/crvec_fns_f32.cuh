@@ -583,21 +583,44 @@ CR_F DD red_trig_dd(float x, int &k) {
 }
 
 // Big-argument lanes of a warp are reduced together (warp-cooperative
-// Payne-Hanek): see ph_cooperative() in the kernel file. This helper is the
-// per-lane body it runs.
+// Payne-Hanek): see coop_payne_hanek() in the kernel file. This helper is the
+// per-lane body it runs, in binary64 arithmetic on the exponent-indexed table
+// PH_T (tools/gen_tables.py gen_ph_table: x * T_j = M * C_j, the bits of
+// 16/pi that matter for this exponent, exact for j < 3):
+//   k0 = RN(x T0), f0 = x T0 - k0 (exact), k1 = RN(f0 + x T1),
+//   s = (f0 - k1) + x T1 (exact, |s| <= 1/2: 53-bit grid), s += x T2 (exact
+//   while |s| < 2^-28), s += x T3; k = k0 + k1
+// x*16/pi has at most ~30 leading zero fraction bits for a binary32 x, so r
+// keeps ~2^-52 relative accuracy (the fast path's budget is 2^-43).
+struct alignas(16) D2 {
+  double x, y;
+};
+#ifndef CRVEC_PH_INT
+CR_F RedTrig ph_reduce(float x, const D2 *tab) {
+  const uint32_t xb = f2u(x);
+  const int row = (int)((xb >> 23) & 0xFFu) - 139;  // 2^12 <= |x| < Inf: 0 .. 115
+  const D2 a = tab[2 * row], b = tab[2 * row + 1];
+  const double xd = f2d(x);
+  const double t = fma_(xd, a.x, SHIFTER);
+  const double kd = sub_(t, SHIFTER);
+  const double f0 = fma_(xd, a.x, -kd);                 // exact, |f0| <= 1/2
+  const double t1 = add_(fma_(xd, a.y, f0), SHIFTER);   // k1 = RN(f0 + x T1)
+  double s = fma_(xd, a.y, sub_(f0, sub_(t1, SHIFTER)));  // exact, |s| <= 1/2
+  s = fma_(xd, b.x, s);
+  s = fma_(xd, b.y, s);
+  return {(int)(d2lo(t) + d2lo(t1)), mul_(s, PI_16_RN)};
+}
+#else
 CR_F RedTrig ph_reduce(float x, const unsigned *words) {
   uint32_t xb = f2u(x);
-  // 128-bit window: x*16/pi has at most ~30 leading zero fraction bits for a
-  // binary32 x, and the window keeps ~99 correct fraction bits (truncating
-  // 1/pi after it perturbs the product by < 2^24 units of its last word).
   PH p = payne_hanek<4>(xb & 0x7FFFFFFFu, words);
-  // 64 + 53 fraction bits: relative accuracy of r even when |r| is tiny.
   double fr = fma_((double)(p.f2 >> 11), 0x1p-53, (double)p.f);
   double r = mul_(fr, PI_16_2M64_H);
   int k = p.k;
   if (xb >> 31) { k = -k; r = -r; }
   return {k, r};
 }
+#endif
 
 // Two register tables: sin(j pi/16) and cos(j pi/16), j = k mod 16. With
 // m = bit 4 of k, sin(x) = (-1)^m (S_j cos r + C_j sin r) and cos(x) =

@@ -96,7 +96,11 @@ struct PHWarp {
   int qx[256];  // queued x bits, overwritten by the reduced k
 };
 struct PHBlock {
-  unsigned words[12];
+#ifndef CRVEC_PH_INT
+  D2 tab[232];  // PH_T
+#else
+  unsigned tab[12];
+#endif
   PHWarp warp[kWarps];
 };
 
@@ -121,7 +125,7 @@ __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bo
   for (int b0 = 0; b0 < total; b0 += 32) {
     int i = b0 + lane;
     if (i < total) {
-      RedTrig r = ph_reduce(u2f((uint32_t)w.qx[i]), sh.words);
+      RedTrig r = ph_reduce(u2f((uint32_t)w.qx[i]), sh.tab);
       w.qx[i] = r.k;
       w.rr[i] = r.r;
     }
@@ -261,7 +265,11 @@ template <class F>
 __device__ __forceinline__ PHBlock *ph_storage() {
   if constexpr (IsTrig<F>::value) {
     __shared__ PHBlock sh;
-    if (threadIdx.x < 12) sh.words[threadIdx.x] = INV_PI_WORDS[threadIdx.x];
+#ifndef CRVEC_PH_INT
+    for (int i = threadIdx.x; i < 232; i += blockDim.x) sh.tab[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
+#else
+    if (threadIdx.x < 12) sh.tab[threadIdx.x] = INV_PI_WORDS[threadIdx.x];
+#endif
     __syncthreads();
     return &sh;
   } else {

@@ -9,6 +9,20 @@
 #include "../../paper_2605_15547_b200/csrc/crvec_fns_f32.cuh"
 using namespace crvec;
 
+#ifdef CRVEC_PH_INT
+static const unsigned *ph_tab() { return INV_PI_WORDS; }
+#else
+static const D2 *ph_tab() {  // PH_T as the kernels' 16-byte pairs
+  static D2 t[232];
+  static bool init = false;
+  if (!init) {
+    for (int i = 0; i < 232; ++i) t[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
+    init = true;
+  }
+  return t;
+}
+#endif
+
 template <class F> struct is_trig : std::false_type {};
 template <int W> struct is_trig<FnTrig<W>> : std::true_type {};
 
@@ -18,7 +32,7 @@ static uint32_t eval1(float x, int force, uint64_t *slow) {
   F::load(R);
   Fast f;
   if constexpr (is_trig<F>::value) {
-    RedTrig q = F::is_big(x) ? ph_reduce(x, INV_PI_WORDS) : red_trig_small(f2d(x));
+    RedTrig q = F::is_big(x) ? ph_reduce(x, ph_tab()) : red_trig_small(f2d(x));
     f = F::from_red(x, q, R);
   } else {
     f = F::fast(x, R);
@@ -82,7 +96,7 @@ static double probe(const uint32_t *x, uint64_t n, uint32_t *E) {
     F::load(R);
     Fast f;
     if constexpr (is_trig<F>::value) {
-      RedTrig q = F::is_big(xf) ? ph_reduce(xf, INV_PI_WORDS) : red_trig_small(f2d(xf));
+      RedTrig q = F::is_big(xf) ? ph_reduce(xf, ph_tab()) : red_trig_small(f2d(xf));
       f = F::from_red(xf, q, R);
     } else {
       f = F::fast(xf, R);

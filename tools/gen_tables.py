@@ -216,6 +216,36 @@ def gen_log():
 
 
 # ----------------------------------------------------------------- trig ----
+def gen_ph_table():
+    """Exponent-indexed Payne-Hanek table for the fast path, |x| >= 2^12.
+
+    x = M * 2^(ex-23) (M < 2^24 an integer): x*16/pi mod 32 = M*C mod 32 with
+    C = (2^(ex-23) * 16/pi) mod 32 -- bits of C of weight >= 32 only add
+    multiples of 32*M. C is cut at 2^-24, 2^-53, 2^-82 into C0 (bits 2^4 ..
+    2^-24, <= 29 bits), C1, C2 (29 bits each) and C3 = RN(rest); the table
+    stores T_j = C_j * 2^-(ex-23), so x * T_j = M * C_j is exact in binary64
+    for j < 3. Row b - 139 for biased exponents b = 139 .. 254."""
+    emit("// Payne-Hanek fast-path table: 4 doubles per binary32 exponent 139..254")
+    rows = []
+    with mp.workprec(1200):
+        pi = mp.pi
+        for b in range(139, 255):
+            sc = mp.mpf(2) ** (b - 127 - 23)
+            c = sc * 16 / pi
+            c = c - 32 * mp.floor(c / 32)
+            parts = []
+            for cut in (24, 53, 82):
+                q = mp.floor(c * mp.mpf(2) ** cut) / mp.mpf(2) ** cut
+                parts.append(q)
+                c -= q
+            parts.append(c)
+            t = [d(q / sc) for q in parts[:3]] + [d(parts[3] / sc)]
+            for j in range(3):  # exact: C_j has <= 29 bits, the scale is a power of two
+                assert mp.mpf(t[j]) * sc == parts[j]
+            rows.extend(t)
+    arr("PH_T", rows)
+
+
 def gen_trig():
     emit("// ---- trig: k = RN(x*16/pi), sin(j*pi/16) table, sin/cos of r ----")
     PI = mp.pi
@@ -248,18 +278,22 @@ def gen_trig():
     scalar("PI_16_Q1", p1); scalar("PI_16_Q2", p2); scalar("PI_16_Q3", p3); scalar("PI_16_Q4", p4)
     # Payne-Hanek: bits of 1/pi, 32-bit words, word w holds bits [32w+1, 32w+32]
     # (bit j has weight 2^-j); 2 zero words of padding in front.
-    v = 1 / PI
-    words = [0, 0]
-    for w in range(10):
-        v = v * (mp.mpf(2) ** 32)
-        iw = int(mp.floor(v))
-        words.append(iw)
-        v -= iw
+    # (320 bits of 1/pi need more than the module's working precision)
+    with mp.workprec(1200):
+        v = 1 / mp.pi
+        words = [0, 0]
+        for w in range(10):
+            v = v * (mp.mpf(2) ** 32)
+            iw = int(mp.floor(v))
+            words.append(iw)
+            v -= iw
     emit("static CR_CONST unsigned INV_PI_WORDS[12] = {")
     emit("    " + ", ".join(f"0x{w:08x}u" for w in words) + ",")
     emit("};")
     hi, lo = dd(PI / 16 * mp.mpf(2) ** -64)
     scalar("PI_16_2M64_H", hi); scalar("PI_16_2M64_L", lo)
+    scalar("PI_16_RN", d(PI / 16))
+    gen_ph_table()
     # slow path: sin/cos Taylor terms (-1)^n / (2n+1)!, (-1)^n / (2n)!
     sn = [mp.mpf((-1) ** n) / mp.factorial(2 * n + 1) for n in range(12)]
     cn = [mp.mpf((-1) ** n) / mp.factorial(2 * n) for n in range(12)]
