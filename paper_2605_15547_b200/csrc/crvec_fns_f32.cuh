@@ -350,6 +350,59 @@ struct FnTanh {
 // x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
 // offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
 // relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
+struct alignas(16) D2 {
+  double x, y;
+};
+
+// Log family: the 16-entry table of (c_i, L_i) pairs lives in shared memory,
+// one LDS.128 per lookup instead of three SHFL (+ a register move to pair the
+// words): 6-16% faster than the register-table form with the shapes re-tuned
+// (profiles/r01/ab_shtab_log.txt). Filled by the block's first 16 threads at
+// kernel entry (every kernel calls F::load() unconditionally in its prologue).
+template <int TAG>
+CR_F const D2 *log_pairs(const double *L) {
+#if CR_DEVICE
+  __shared__ D2 tab[16];
+  if (threadIdx.x < 16) tab[threadIdx.x] = D2{hilo2d(LOG_C_HI[threadIdx.x], 0u), L[threadIdx.x]};
+  __syncthreads();
+  return tab;
+#else
+  static D2 tab[16];
+  for (int i = 0; i < 16; ++i) tab[i] = D2{hilo2d(LOG_C_HI[i], 0u), L[i]};
+  return tab;
+#endif
+}
+
+// Generic shared 16-entry table: entry i = {A[i], B[i]} (+ optional third
+// value hilo2d(W[i], 0) at +16 B: 32-byte entries), same fill rule as above.
+template <int TAG, bool THIRD>
+CR_F const D2 *sh_table16(const double *A, const double *B, const int *W) {
+#if CR_DEVICE
+  __shared__ D2 tab[THIRD ? 32 : 16];
+  if (threadIdx.x < 16) {
+    if (THIRD) {
+      tab[2 * threadIdx.x] = D2{A[threadIdx.x], B[threadIdx.x]};
+      tab[2 * threadIdx.x + 1] = D2{hilo2d(W[threadIdx.x], 0u), 0.0};
+    } else {
+      tab[threadIdx.x] = D2{A[threadIdx.x], B[threadIdx.x]};
+    }
+  }
+  __syncthreads();
+  return tab;
+#else
+  static D2 tab[THIRD ? 32 : 16];
+  for (int i = 0; i < 16; ++i) {
+    if (THIRD) {
+      tab[2 * i] = D2{A[i], B[i]};
+      tab[2 * i + 1] = D2{hilo2d(W[i], 0u), 0.0};
+    } else {
+      tab[i] = D2{A[i], B[i]};
+    }
+  }
+  return tab;
+#endif
+}
+
 struct RedLog {
   int e, i;
   double m;
@@ -367,17 +420,15 @@ CR_F RedLog red_log(double xd) {
 template <int BASE>  // 0: ln, 2: log2, 10: log10
 struct FnLogB {
   static constexpr uint32_t E = 1024;
-  struct Regs { int c; double l; };
+  struct Regs { const D2 *t; };
   CR_F static void load(Regs &R) {
-    R.c = CR_TAB_LOAD(LOG_C_HI);
-    R.l = BASE == 0 ? CR_TAB_LOAD(LOG_L_HI) : BASE == 2 ? CR_TAB_LOAD(LOG2_L_HI) : CR_TAB_LOAD(LOG10_L_HI);
+    R.t = log_pairs<BASE>(BASE == 0 ? LOG_L_HI : BASE == 2 ? LOG2_L_HI : LOG10_L_HI);
   }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedLog q = red_log(f2d(x));
-    double c = hilo2d(CR_TAB(R.c, LOG_C_HI, q.i), 0u);  // c_i has <= 21 significant bits
-    double L = BASE == 0 ? CR_TAB(R.l, LOG_L_HI, q.i)
-                         : BASE == 2 ? CR_TAB(R.l, LOG2_L_HI, q.i) : CR_TAB(R.l, LOG10_L_HI, q.i);
+    const D2 cl = R.t[q.i & 15];
+    const double c = cl.x, L = cl.y;
     double r = fma_(q.m, c, -1.0);  // exact
     double p = fma_(mul_(r, r), logq(r), r);
     double ed = i2d(q.e), a;
@@ -420,17 +471,14 @@ using FnLog10 = FnLogB<10>;
 
 struct FnLog1p {
   static constexpr uint32_t E = 1024;
-  struct Regs { int c; double l; };
-  CR_F static void load(Regs &R) {
-    R.c = CR_TAB_LOAD(LOG_C_HI);
-    R.l = CR_TAB_LOAD(LOG_L_HI);
-  }
+  struct Regs { const D2 *t; };
+  CR_F static void load(Regs &R) { R.t = log_pairs<1>(LOG_L_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     double y = add_(1.0, f2d(x));
     RedLog q = red_log(y);
-    double c = hilo2d(CR_TAB(R.c, LOG_C_HI, q.i), 0u);
-    double L = CR_TAB(R.l, LOG_L_HI, q.i);
+    const D2 cl = R.t[q.i & 15];
+    const double c = cl.x, L = cl.y;
     double r = fma_(q.m, c, -1.0);
     double p = fma_(mul_(r, r), logq(r), r);
     double a = add_(fma_(i2d(q.e), LN2_D, L), p);
@@ -592,9 +640,6 @@ CR_F DD red_trig_dd(float x, int &k) {
 //   while |s| < 2^-28), s += x T3; k = k0 + k1
 // x*16/pi has at most ~30 leading zero fraction bits for a binary32 x, so r
 // keeps ~2^-52 relative accuracy (the fast path's budget is 2^-43).
-struct alignas(16) D2 {
-  double x, y;
-};
 #ifndef CRVEC_PH_INT
 CR_F RedTrig ph_reduce(float x, const D2 *tab) {
   const uint32_t xb = f2u(x);
@@ -622,26 +667,23 @@ CR_F RedTrig ph_reduce(float x, const unsigned *words) {
 }
 #endif
 
-// Two register tables: sin(j pi/16) and cos(j pi/16), j = k mod 16. With
-// m = bit 4 of k, sin(x) = (-1)^m (S_j cos r + C_j sin r) and cos(x) =
-// (-1)^m (C_j cos r - S_j sin r): one sign flip of the result (none for tan).
-struct TrigRegs {
-  double s, c;
-};
+// One 16-entry shared table of (sin(j pi/16), cos(j pi/16)) pairs, j = k mod
+// 16, read with one LDS.128 (5-8% faster than two register tables read with
+// four SHFL: profiles/r01/ab_shtab_trig.txt). With m = bit 4 of k,
+// sin(x) = (-1)^m (S_j cos r + C_j sin r) and cos(x) = (-1)^m (C_j cos r -
+// S_j sin r): one sign flip of the result (none for tan).
 CR_F double flip_k16(double v, int k) { return hilo2d(d2hi(v) ^ ((k << 27) & (int)0x80000000), d2lo(v)); }
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
   static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
   static constexpr bool kBigArg = true;
-  using Regs = TrigRegs;
-  CR_F static void load(Regs &R) {
-    R.s = CR_TAB_LOAD(SIN16_HI);
-    R.c = CR_TAB_LOAD(COS16_HI);
-  }
+  struct Regs { const D2 *t; };
+  CR_F static void load(Regs &R) { R.t = sh_table16<100, false>(SIN16_HI, COS16_HI, nullptr); }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    double Sj = CR_TAB(R.s, SIN16_HI, q.k), Cj = CR_TAB(R.c, COS16_HI, q.k);
+    const D2 sc = R.t[q.k & 15];
+    const double Sj = sc.x, Cj = sc.y;
     double a;
     if (WHICH == 0) a = flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k);
     else if (WHICH == 1) a = flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k);
@@ -657,7 +699,8 @@ struct FnTrig {
   CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    double Sj = CR_TAB(R.s, SIN16_HI, q.k), Cj = CR_TAB(R.c, COS16_HI, q.k);
+    const D2 sc = R.t[q.k & 15];
+    const double Sj = sc.x, Cj = sc.y;
     const uint32_t xb = f2u(x);
     fs = Fast{flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k), FnTrig<0>::in_main(xb)};
     fc = Fast{flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k), FnTrig<1>::in_main(xb)};
@@ -742,20 +785,16 @@ CR_F double atan_t2(double t) {
 
 struct FnAtan {
   static constexpr uint32_t E = 512;
-  struct Regs { int a; double c, s; };
-  CR_F static void load(Regs &R) {
-    R.a = CR_TAB_LOAD(ATAN_A_HI);
-    R.c = CR_TAB_LOAD(ATAN_C);
-    R.s = CR_TAB_LOAD(ATAN_S);
-  }
+  struct Regs { const D2 *t; };
+  CR_F static void load(Regs &R) { R.t = sh_table16<101, true>(ATAN_C, ATAN_S, ATAN_A_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     float axf = fminf(fabs_(x), 0x1p127f);
     double z = f2d(axf);
     bool up = axf > 1.0f;
     int k = (int)f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f)) + (up ? 8 : 0);
-    double A = hilo2d(CR_TAB(R.a, ATAN_A_HI, k), 0u);
-    double C = CR_TAB(R.c, ATAN_C, k), S = CR_TAB(R.s, ATAN_S, k);
+    const D2 cs = R.t[2 * (k & 15)];
+    const double A = R.t[2 * (k & 15) + 1].x, C = cs.x, S = cs.y;
     double t = div_fast(fma_(z, C, -S), fma_(z, S, C));
     return Fast{with_sign(add_(A, atan_t2(t)), xb), in_main(xb)};
   }

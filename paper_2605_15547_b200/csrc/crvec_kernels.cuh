@@ -307,15 +307,16 @@ template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, m
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 4, nv = 2, minb = 2; };
-template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 3; };
-template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 4; };
+template <> struct KernelShape<FnLog> { static constexpr int vw = 4, nv = 2, minb = 4; };
+template <> struct KernelShape<FnLog2> { static constexpr int vw = 4, nv = 2, minb = 4; };
 template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnLog10> { static constexpr int vw = 4, nv = 2, minb = 4; };
-template <> struct KernelShape<FnAtan> { static constexpr int vw = 4, nv = 2, minb = 2; };
+template <> struct KernelShape<FnAtan> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
-template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 4, nv = 2, minb = 2; };
+template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 8, nv = 1, minb = 3; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step
 // into `nxt`, evaluate `cur`, store. Called alternately with the two register
@@ -515,7 +516,7 @@ __device__ __forceinline__ void sincos_step(const float4 *__restrict__ x, float4
     sincos_rare_store<M, 4 * NV>(xs, mask, (float *)ys, (float *)yc, 4u * base, counters);
 }
 
-constexpr int kSincosNV = 2, kSincosMinB = 2;
+constexpr int kSincosNV = 2, kSincosMinB = 3;
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, kSincosMinB)

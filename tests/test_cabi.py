@@ -83,10 +83,16 @@ def test_kernels_compiled_for_sm100a():
     so = os.path.join(ROOT, "paper_2605_15547_b200", "libcrvec.so")
     out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPKfPfjPy", so],
-                          capture_output=True, text=True).stdout
-    for op in ("DFMA", "SHFL.IDX", "LDG.E.NA", "STG.E.EF", "F2F.F32.F64"):
-        assert op in sass, op
+    def sass(fn):
+        return subprocess.run(["cuobjdump", "-sass", "-fun", fn, so], capture_output=True, text=True).stdout
+    # logf: shared-memory (c, L) table read with one LDS.128 per element
+    s = sass("_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPKfPfjPy")
+    for op in ("DFMA", "LDS.128", "LDG.E.NA", "STG.E.EF", "F2F.F32.F64"):
+        assert op in s, op
+    # expf: register table read with __shfl_sync
+    s = sass("_ZN5crvec9k_map_vecINS_5FnExpELi0EEEvPKfPfjPy")
+    for op in ("DFMA", "SHFL.IDX", "LDG.E", "STG.E", "F2F.F32.F64"):
+        assert op in s, op
 
 
 def test_cpp_compat_header_compiles(lib, tmp_path):

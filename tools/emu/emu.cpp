@@ -38,6 +38,9 @@ static uint32_t eval1(float x, int force, uint64_t *slow) {
     f = F::fast(x, R);
   }
   if (!f.main) return F::template special<M>(x);
+  if constexpr (std::is_same<F, FnLog1p>::value) {
+    if (!force && F::is_tiny(f2u(x))) return F::template tiny_bits<M>(f2u(x));  // kernels' rule
+  }
   bool fail;
   uint32_t y = finish<M>(f, fail, F::E);
   if (fail || force) {
