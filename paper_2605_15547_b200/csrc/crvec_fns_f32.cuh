@@ -18,6 +18,12 @@
 
 namespace crvec {
 
+// A 16-byte pair: one LDS.128 reads both halves of a shared-table entry.
+struct alignas(16) D2 {
+  double x, y;
+};
+
+
 
 // Polynomials (Horner, coefficients from tools/gen_tables.py).
 CR_F double expq(double r) {
@@ -37,9 +43,26 @@ CR_F double with_sign(double a, uint32_t xb) {
 }
 
 // ============================================================ exp family ====
+// The 2^(j/16) table: shared memory (one LDS.64 per lookup; exp, exp10, tanh:
+// +1..5%) or registers (two SHFL; exp2 neutral, expm1 -3.5% in shared form),
+// per function by measurement (profiles/r01/ab_shtab_exp.txt).
+template <int TAG>
+CR_F const double *exp_tab() {
+#if CR_DEVICE
+  __shared__ double tab[16];
+  if (threadIdx.x < 16) tab[threadIdx.x] = EXP2J_HI[threadIdx.x];
+  __syncthreads();
+  return tab;
+#else
+  return EXP2J_HI;
+#endif
+}
+CR_F double exp_t(const double *tab, int k) { return tab[k & 15]; }
+CR_F double exp_t(double reg, int k) { return CR_TAB(reg, EXP2J_HI, k); }  // lane k mod 32 -> entry k & 15
 // exp_core: 2^(k/16) * e^r with |r| <= ln2/32 (fast path).
-CR_F double exp_core(int k, double r, double tab) {
-  double T = CR_TAB(tab, EXP2J_HI, k);  // shfl: source lane k mod 32 -> entry k & 15
+template <class Tab>
+CR_F double exp_core(int k, double r, Tab tab) {
+  double T = exp_t(tab, k);
   double p = fma_(mul_(r, r), expq(r), r);  // e^r - 1
   return scale2(fma_(T, p, T), k >> 4);
 }
@@ -47,8 +70,9 @@ CR_F double exp_core(int k, double r, double tab) {
 // Cubic-Q variant (2^-40.1 relative on e^r - 1, i.e. < 2^-45.5 on the
 // result): the rounding-test tolerance E = 512 covers it with margin.
 CR_F double expq3(double r) { return fma_(fma_(fma_(EXPQ3[3], r, EXPQ3[2]), r, EXPQ3[1]), r, EXPQ3[0]); }
-CR_F double exp_core3(int k, double r, double tab) {
-  double T = CR_TAB(tab, EXP2J_HI, k);  // shfl: source lane k mod 32 -> entry k & 15
+template <class Tab>
+CR_F double exp_core3(int k, double r, Tab tab) {
+  double T = exp_t(tab, k);
   double p = fma_(mul_(r, r), expq3(r), r);  // e^r - 1
   return scale2(fma_(T, p, T), k >> 4);
 }
@@ -100,8 +124,8 @@ CR_F DD red_exp_dd(double xc, int &k) {
 
 struct FnExp {
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = exp_tab<121>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -104.5f), 89.5f)));
     // main: 2^-26 < |x| < inf (saturation is handled by the clamp)
@@ -147,8 +171,8 @@ struct FnExp2 {
 
 struct FnExp10 {
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = exp_tab<123>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     double xc = f2d(fminf(fmaxf(x, -45.5f), 39.5f));
     double t = fma_(xc, LOG2_10_16, SHIFTER);
@@ -184,7 +208,7 @@ struct FnExpm1 {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -18.5f), 89.5f)));
     int e = q.k >> 4;
-    double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
+    double T = scale2(exp_t(R.t, q.k), e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     // main: 2^-26 < |x| < inf and x >= -18
     return Fast{fma_(T, p, sub_(T, 1.0)), in_main(xb)};
@@ -223,12 +247,30 @@ struct HypParts {
 };
 // Fast path uses the rounded table (2^-54 relative per entry): for k = +-1 the
 // difference E+ - E- loses ~5 bits, which the sinh/tanh tolerances cover.
-CR_F HypParts hyp_parts(double ax, double tab) {
+// Shared table of (2^(j/16), 2^(-j/16 mod 1)) pairs: e^(+a) and e^(-a) come
+// from one LDS.128 (entry k mod 16 holds T[k mod 16] and T[-k mod 16]); 4-5%
+// faster than four SHFL (profiles/r01/ab_shtab_hyp.txt).
+template <int TAG>
+CR_F const D2 *exp_pm_pairs() {
+#if CR_DEVICE
+  __shared__ D2 tab[16];
+  if (threadIdx.x < 16) tab[threadIdx.x] = D2{EXP2J_HI[threadIdx.x], EXP2J_HI[(16 - threadIdx.x) & 15]};
+  __syncthreads();
+  return tab;
+#else
+  static D2 tab[16];
+  for (int i = 0; i < 16; ++i) tab[i] = D2{EXP2J_HI[i], EXP2J_HI[(16 - i) & 15]};
+  return tab;
+#endif
+}
+using HypTab = const D2 *;
+CR_F HypParts hyp_parts(double ax, HypTab tab) {
   RedExp q = red_exp(ax);
   int kp = q.k, km = -q.k;
   // e^(+-a)/2: the halving folds into the integer exponent add
-  double Ep = scale2(CR_TAB(tab, EXP2J_HI, kp), (kp >> 4) - 1);
-  double Em = scale2(CR_TAB(tab, EXP2J_HI, km), (km >> 4) - 1);
+  const D2 pm = tab[kp & 15];
+  double Ep = scale2(pm.x, (kp >> 4) - 1);
+  double Em = scale2(pm.y, (km >> 4) - 1);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(SINHQ[1], s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(COSHQ[1], s, COSHQ[0]), 1.0);
@@ -260,8 +302,8 @@ CR_F HypDD hyp_parts_dd(double ax) {
 
 struct FnSinh {
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { HypTab t; };
+  CR_F static void load(Regs &R) { R.t = exp_pm_pairs<110>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
@@ -286,8 +328,8 @@ struct FnSinh {
 
 struct FnCosh {
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { HypTab t; };
+  CR_F static void load(Regs &R) { R.t = exp_pm_pairs<111>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     HypParts h = hyp_parts(f2d(fminf(fabs_(x), 90.0f)), R.t);
     return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)), in_main(f2u(x))};
@@ -311,13 +353,13 @@ struct FnTanh {
   // tanh|x| = E / (E + 2), E = expm1(2|x|) = T (1 + p) - 1 (T rounded: for
   // k = +-1 the cancellation costs ~2^-49.5, covered by E).
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = exp_tab<125>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(mul_(2.0, f2d(fminf(fabs_(x), 10.0f))));
     int e = q.k >> 4;
-    double T = scale2(CR_TAB(R.t, EXP2J_HI, q.k), e);
+    double T = scale2(exp_t(R.t, q.k), e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     double em1 = fma_(T, p, sub_(T, 1.0));
     return Fast{with_sign(div_fast(em1, add_(em1, 2.0)), xb), in_main(xb)};
@@ -350,10 +392,6 @@ struct FnTanh {
 // x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
 // offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
 // relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
-struct alignas(16) D2 {
-  double x, y;
-};
-
 // Log family: the 16-entry table of (c_i, L_i) pairs lives in shared memory,
 // one LDS.128 per lookup instead of three SHFL (+ a register move to pair the
 // words): 6-16% faster than the register-table form with the shapes re-tuned
