@@ -869,11 +869,10 @@ CR_F double asinq(double d) {
 template <bool ACOS>
 struct FnAsinAcos {
   static constexpr uint32_t E = 64;
-  struct Regs { int a; double c, s; };
+  struct Regs { int a; const D2 *t; };
   CR_F static void load(Regs &R) {
     R.a = ACOS ? CR_TAB_LOAD(ACOS_A_HI) : CR_TAB_LOAD(ASIN_A_HI);
-    R.c = ACOS ? CR_TAB_LOAD(ACOS_C) : CR_TAB_LOAD(ASIN_C);
-    R.s = ACOS ? CR_TAB_LOAD(ACOS_S) : CR_TAB_LOAD(ASIN_S);
+    R.t = ACOS ? sh_table16<102, false>(ACOS_C, ACOS_S, nullptr) : sh_table16<103, false>(ASIN_C, ASIN_S, nullptr);
   }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
@@ -883,11 +882,13 @@ struct FnAsinAcos {
     float sf = (float)s;
     bool up = axf > sf;
     // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; the
-    // shuffle reads lane k mod 32 (table replicated in both half-warps)
+    // angle is a register table (one SHFL, lane k mod 32), (cos, sin) a
+    // shared pair (one LDS.128): +6% over five SHFL, and over 32-byte shared
+    // entries (profiles/r01/ab_shtab_trig.txt)
     int k = (int)f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f)) + (up ? 8 : 0);
     double A = hilo2d(ACOS ? CR_TAB(R.a, ACOS_A_HI, k) : CR_TAB(R.a, ASIN_A_HI, k), 0u);
-    double C = ACOS ? CR_TAB(R.c, ACOS_C, k) : CR_TAB(R.c, ASIN_C, k);
-    double S = ACOS ? CR_TAB(R.s, ACOS_S, k) : CR_TAB(R.s, ASIN_S, k);
+    const D2 cs = R.t[k & 15];
+    const double C = cs.x, S = cs.y;
     double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
     double a = add_(A, asinq(d));
     if (!ACOS) a = with_sign(a, xb);

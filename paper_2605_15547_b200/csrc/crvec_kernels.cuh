@@ -315,7 +315,7 @@ template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 1, mi
 template <> struct KernelShape<FnLog10> { static constexpr int vw = 4, nv = 2, minb = 4; };
 template <> struct KernelShape<FnAtan> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 8, nv = 1, minb = 4; };
-template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 4, nv = 1, minb = 4; };
+template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 8, nv = 1, minb = 3; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step
