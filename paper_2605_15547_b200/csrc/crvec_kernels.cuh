@@ -310,10 +310,10 @@ template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 1, mi
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog2> { static constexpr int vw = 8, nv = 2, minb = 2; };
-template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 1, minb = 3; };
-template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 2, minb = 2; };
+template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog10> { static constexpr int vw = 8, nv = 2, minb = 2; };
-template <> struct KernelShape<FnAtan> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <> struct KernelShape<FnAtan> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 8, nv = 1, minb = 3; };
