@@ -107,6 +107,7 @@ struct PHBlock {
 template <int NE>
 __device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bool (&big)[NE],
                                                  RedTrig (&q)[NE], PHBlock &sh) {
+  static_assert(32 * NE <= 256, "PHWarp holds 32 x 8 queued arguments");
   const int lane = threadIdx.x & 31;
   PHWarp &w = sh.warp[threadIdx.x >> 5];
   const unsigned lt = (1u << lane) - 1u;
@@ -464,18 +465,19 @@ constexpr bool kSincosStore = true;
 
 // Store form of the sincosf rare path (after both vector stores): scalar
 // overwrite of the one sin or cos output a pending bit names.
-template <int M, int NE>
+template <int M, int NE, int VW>
 __device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigned mask, float *ys,
                                                   float *yc, uint32_t fbase,
                                                   unsigned long long *counters) {
+  static_assert(NE <= 16 && (NE & (NE - 1)) == 0, "NE: power of two, <= 16 (16-bit halves)");
   int cnt = 0;
   do {
     const unsigned low = mask & (0u - mask);
     const unsigned slot = (low | (low >> 16)) & 0xFFFFu;
     const float xe = gather_slot<NE>(xs, slot);
     if (low) {
-      const uint32_t e = ((uint32_t)__ffs(low) - 1u) & 15u;
-      const uint32_t fi = fbase + 128u * (e >> 2) + (e & 3u);
+      const uint32_t e = ((uint32_t)__ffs(low) - 1u) & (NE - 1u);
+      const uint32_t fi = fbase + 32u * VW * (e / VW) + (e % VW);
       if (low >> 16) yc[fi] = u2f(resolve_one<FnCos, M>(xe, cnt));
       else ys[fi] = u2f(resolve_one<FnSin, M>(xe, cnt));
     }
@@ -484,63 +486,70 @@ __device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigne
   if (cnt) atomicAdd(counters, (unsigned long long)cnt);
 }
 
-template <int M, int NV>
-__device__ __forceinline__ void sincos_step(const float4 *__restrict__ x, float4 *__restrict__ ys,
-                                            float4 *__restrict__ yc, uint32_t n4, uint32_t base,
-                                            uint32_t stride, const float4 (&cur)[NV],
-                                            float4 (&nxt)[NV], const FnSin::Regs &R, PHBlock *sh,
+template <int M, int VW, int NV>
+__device__ __forceinline__ void sincos_step(const Vec<VW> *__restrict__ x, Vec<VW> *__restrict__ ys,
+                                            Vec<VW> *__restrict__ yc, uint32_t nv, uint32_t base,
+                                            uint32_t stride, const Vec<VW> (&cur)[NV],
+                                            Vec<VW> (&nxt)[NV], const FnSin::Regs &R, PHBlock *sh,
                                             unsigned long long *counters) {
-  float xs[4 * NV];
+  float xs[VW * NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t in = base + stride + 32 * k;
-    if (in < n4) nxt[k] = ld_stream(x + in);
-    xs[4 * k] = cur[k].x;
-    xs[4 * k + 1] = cur[k].y;
-    xs[4 * k + 2] = cur[k].z;
-    xs[4 * k + 3] = cur[k].w;
+    if (in < nv) nxt[k] = ld_vec<VW>(x + in);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) xs[VW * k + j] = cur[k].v[j];
   }
-  uint32_t s[4 * NV], c[4 * NV];
-  unsigned mask = sincos_lanes<M, 4 * NV, kSincosStore>(xs, s, c, R, sh, counters);
+  uint32_t s[VW * NV], c[VW * NV];
+  unsigned mask = sincos_lanes<M, VW * NV, kSincosStore>(xs, s, c, R, sh, counters);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = base + 32 * k;
-    if (i < n4) {
-      st_stream(ys + i, make_float4(u2f(s[4 * k]), u2f(s[4 * k + 1]), u2f(s[4 * k + 2]), u2f(s[4 * k + 3])));
-      st_stream(yc + i, make_float4(u2f(c[4 * k]), u2f(c[4 * k + 1]), u2f(c[4 * k + 2]), u2f(c[4 * k + 3])));
+    if (i < nv) {
+      st_vec<VW>(ys + i, s + VW * k);
+      st_vec<VW>(yc + i, c + VW * k);
     } else {
-      mask &= ~((15u << (4 * k)) | (15u << (4 * k + 16)));  // stale inputs past the end
+      constexpr unsigned kv = (1u << VW) - 1u;
+      mask &= ~((kv << (VW * k)) | (kv << (VW * k + 16)));  // stale inputs past the end
     }
   }
   if (kSincosStore && __any_sync(kFull, mask != 0))
-    sincos_rare_store<M, 4 * NV>(xs, mask, (float *)ys, (float *)yc, 4u * base, counters);
+    sincos_rare_store<M, VW * NV, VW>(xs, mask, (float *)ys, (float *)yc, VW * base, counters);
 }
 
-constexpr int kSincosNV = 2, kSincosMinB = 3;
+#ifndef CRVEC_SINCOS_SHAPE
+#define CRVEC_SINCOS_SHAPE 8, 1, 3  // vw, nv, minb (profiles/r01/ab_shtab_trig.txt)
+#endif
+constexpr int kSincosShape[3] = {CRVEC_SINCOS_SHAPE};
+constexpr int kSincosVW = kSincosShape[0], kSincosNV = kSincosShape[1], kSincosMinB = kSincosShape[2];
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, kSincosMinB)
-    k_sincos_vec(const float4 *__restrict__ x, float4 *__restrict__ ys, float4 *__restrict__ yc,
-                 uint32_t n4, unsigned long long *counters) {
-  constexpr int NV = kSincosNV;
+    k_sincos_vec(const float *__restrict__ xf, float *__restrict__ ysf, float *__restrict__ ycf,
+                 uint32_t nv, unsigned long long *counters) {
+  constexpr int VW = kSincosVW, NV = kSincosNV;
+  const Vec<VW> *x = reinterpret_cast<const Vec<VW> *>(xf);
+  Vec<VW> *ys = reinterpret_cast<Vec<VW> *>(ysf);
+  Vec<VW> *yc = reinterpret_cast<Vec<VW> *>(ycf);
   PHBlock *sh = ph_storage<FnSin>();
   FnSin::Regs R;
   FnSin::load(R);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * (uint32_t)(kThreads * NV);
   uint32_t base = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 * NV) + lane;
-  float4 va[NV], vb[NV];
+  Vec<VW> va[NV], vb[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    va[k] = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) va[k].v[j] = 1.f;
     vb[k] = va[k];
-    if (base + 32 * k < n4) va[k] = ld_stream(x + base + 32 * k);
+    if (base + 32 * k < nv) va[k] = ld_vec<VW>(x + base + 32 * k);
   }
-  while (base - lane < n4) {
-    sincos_step<M, NV>(x, ys, yc, n4, base, stride, va, vb, R, sh, counters);
+  while (base - lane < nv) {
+    sincos_step<M, VW, NV>(x, ys, yc, nv, base, stride, va, vb, R, sh, counters);
     base += stride;
-    if (base - lane >= n4) break;
-    sincos_step<M, NV>(x, ys, yc, n4, base, stride, vb, va, R, sh, counters);
+    if (base - lane >= nv) break;
+    sincos_step<M, VW, NV>(x, ys, yc, nv, base, stride, vb, va, R, sh, counters);
     base += stride;
   }
 }
@@ -838,20 +847,33 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
 template <int M>
 cudaError_t launch_sincos(const float *x, float *ys, float *yc, uint64_t n, cudaStream_t s,
                           unsigned long long *ctr) {
+  constexpr int VW = kSincosVW, NV = kSincosNV;
   static int mb_vec = max_blocks(k_sincos_vec<M>);
   static int mb_sc = max_blocks(k_sincos_scalar<M>);
-  bool aligned = (((uintptr_t)x | (uintptr_t)ys | (uintptr_t)yc) & 15) == 0;
-  uint64_t n4 = aligned ? n / 4 : 0;
-  constexpr uint64_t kMaxN4 = uint64_t(1) << 31;
-  for (uint64_t off = 0; off < n4; off += kMaxN4) {
-    uint64_t m = n4 - off < kMaxN4 ? n4 - off : kMaxN4;
-    k_sincos_vec<M><<<grid_for((m + 32 * kSincosNV - 1) / (32 * kSincosNV), mb_vec), kThreads, 0, s>>>(
-        (const float4 *)x + off, (float4 *)ys + off, (float4 *)yc + off, (uint32_t)m, ctr);
+  constexpr uintptr_t A = 4 * VW - 1;
+  auto scalar = [&](uint64_t off, uint64_t m) {
+    if (m)
+      k_sincos_scalar<M><<<grid_for((m + 31) / 32, mb_sc), kThreads, 0, s>>>(x + off, ys + off, yc + off,
+                                                                               m, ctr);
+  };
+  // the three arrays equally misaligned: peel a scalar head to the vector boundary
+  uint64_t head = 0;
+  const uintptr_t ax = (uintptr_t)x & A;
+  if (((uintptr_t)ys & A) == ax && ((uintptr_t)yc & A) == ax && (ax & 3) == 0 && ax)
+    head = ((A + 1 - ax) & A) / 4;
+  if (head > n) head = n;
+  const bool aligned = ((((uintptr_t)(x + head)) | ((uintptr_t)(ys + head)) | ((uintptr_t)(yc + head))) & A) == 0;
+  const uint64_t nvec = aligned ? (n - head) / VW : 0;
+  const uint64_t v0 = aligned ? head : 0;
+  scalar(0, v0);
+  constexpr uint64_t kMaxNV = uint64_t(1) << 31;
+  for (uint64_t off = 0; off < nvec; off += kMaxNV) {
+    uint64_t m = nvec - off < kMaxNV ? nvec - off : kMaxNV;
+    const uint64_t f = v0 + VW * off;
+    k_sincos_vec<M><<<grid_for((m + 32 * NV - 1) / (32 * NV), mb_vec), kThreads, 0, s>>>(
+        x + f, ys + f, yc + f, (uint32_t)m, ctr);
   }
-  uint64_t rem = n - 4 * n4;
-  if (rem)
-    k_sincos_scalar<M><<<grid_for((rem + 31) / 32, mb_sc), kThreads, 0, s>>>(
-        x + 4 * n4, ys + 4 * n4, yc + 4 * n4, rem, ctr);
+  scalar(v0 + VW * nvec, n - (v0 + VW * nvec));
   return cudaGetLastError();
 }
 
