@@ -43,9 +43,9 @@ CR_F double with_sign(double a, uint32_t xb) {
 }
 
 // ============================================================ exp family ====
-// The 2^(j/16) table: shared memory (one LDS.64 per lookup; exp, exp10, tanh:
-// +1..5%) or registers (two SHFL; exp2 neutral, expm1 -3.5% in shared form),
-// per function by measurement (profiles/r01/ab_shtab_exp.txt).
+// The 2^(j/16) table: shared memory, one LDS.64 per lookup instead of two SHFL
+// (+1..5% with the shapes re-tuned, profiles/r01/ab_shtab_exp.txt). The
+// register form (exp_t(double, k)) stays for the emulation build and A/B.
 template <int TAG>
 CR_F const double *exp_tab() {
 #if CR_DEVICE
@@ -144,8 +144,8 @@ struct FnExp {
 
 struct FnExp2 {
   static constexpr uint32_t E = 512;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = exp_tab<130>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     double xc = f2d(fminf(fmaxf(x, -151.5f), 129.5f));
     double t = fma_(xc, 16.0, SHIFTER);
@@ -202,8 +202,8 @@ struct FnExp10 {
 
 struct FnExpm1 {
   static constexpr uint32_t E = 128;
-  struct Regs { double t; };
-  CR_F static void load(Regs &R) { R.t = CR_TAB_LOAD(EXP2J_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = exp_tab<131>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -18.5f), 89.5f)));

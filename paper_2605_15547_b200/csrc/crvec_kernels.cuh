@@ -303,10 +303,10 @@ template <class F>
 struct KernelShape {
   static constexpr int vw = 4, nv = 2, minb = 3;
 };
-template <> struct KernelShape<FnExp2> { static constexpr int vw = 4, nv = 4, minb = 2; };
+template <> struct KernelShape<FnExp2> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
-template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 1, minb = 4; };
+template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 2, minb = 3; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 4; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 2, minb = 2; };

@@ -89,8 +89,8 @@ def test_kernels_compiled_for_sm100a():
     s = sass("_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPKfPfjPy")
     for op in ("DFMA", "LDS.128", "LDG.E.NA", "STG.E.EF", "F2F.F32.F64"):
         assert op in s, op
-    # exp2f: register table read with __shfl_sync
-    s = sass("_ZN5crvec9k_map_vecINS_6FnExp2ELi0EEEvPKfPfjPy")
+    # asinf: angle from a register table read with __shfl_sync
+    s = sass("_ZN5crvec9k_map_vecINS_10FnAsinAcosILb0EEELi0EEEvPKfPfjPy")
     for op in ("DFMA", "SHFL.IDX", "LDG.E", "STG.E", "F2F.F32.F64"):
         assert op in s, op
 
