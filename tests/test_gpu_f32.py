@@ -200,3 +200,23 @@ def test_offset_pointers_head_peel(cuda, oracle, name, ox, oy):
     crvec.eval_f32(name, bx[ox:ox + n], 0, out=by[oy:oy + n])
     ex, nbad = _mismatch_report(x, by[oy:oy + n].cpu().numpy().view(np.uint32), want)
     assert nbad == 0, f"{name} ({ox},{oy}): {ex}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ox,oy,oc", [(0, 0, 0), (1, 1, 1), (3, 3, 3), (5, 5, 5), (1, 0, 1), (2, 2, 0)])
+def test_sincosf_offset_pointers_head_peel(cuda, oracle, ox, oy, oc):
+    """sincosf with its three arrays offset from a 256-byte boundary: equal
+    offsets peel a scalar head to the 256-bit boundary, any unequal offset
+    takes the element kernel; both outputs match sinf / cosf of the oracle."""
+    n = (1 << 18) + 5
+    x = np.concatenate([trig_input(n // 2), mixed_f32("sincosf", n)])[:n]
+    want_s = oracle.f32(crvec.ORACLE_NAME["sinf"], x, 0)
+    want_c = oracle.f32(crvec.ORACLE_NAME["cosf"], x, 0)
+    bx = cuda.zeros(n + 8, dtype=cuda.float32, device="cuda")
+    bs = cuda.zeros(n + 8, dtype=cuda.float32, device="cuda")
+    bc = cuda.zeros(n + 8, dtype=cuda.float32, device="cuda")
+    bx[ox:ox + n] = cuda.from_numpy(x.view(np.float32)).cuda()
+    crvec.eval_f32("sincosf", bx[ox:ox + n], 0, out=bs[oy:oy + n], out2=bc[oc:oc + n])
+    for got, want, what in ((bs[oy:oy + n], want_s, "sin"), (bc[oc:oc + n], want_c, "cos")):
+        ex, nbad = _mismatch_report(x, got.cpu().numpy().view(np.uint32), want)
+        assert nbad == 0, f"sincosf {what} ({ox},{oy},{oc}): {ex}"
