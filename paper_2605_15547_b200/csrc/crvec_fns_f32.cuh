@@ -1,6 +1,7 @@
 // The 19 correctly rounded binary32 functions of the paper (ref: PAPER.md:49):
-// fast path (branch-free fp64 range reduction + <=16-entry register table via
-// __shfl_sync + fp64 polynomial + one static-mode conversion) and a rare
+// fast path (branch-free fp64 range reduction + <=16-entry table held in
+// shared memory or in registers read with __shfl_sync, per function by
+// measurement + fp64 polynomial + one static-mode conversion) and a rare
 // double-double accurate path for lanes the rounding test cannot decide.
 //
 // The reference implements exp2f / log2f only (ref: proj/src/kernels_f32.cpp:
@@ -389,9 +390,6 @@ struct FnTanh {
 };
 
 // ============================================================ log family ====
-// x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
-// offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
-// relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
 // Log family: the 16-entry table of (c_i, L_i) pairs lives in shared memory,
 // one LDS.128 per lookup instead of three SHFL (+ a register move to pair the
 // words): 6-16% faster than the register-table form with the shapes re-tuned
@@ -441,13 +439,15 @@ CR_F const D2 *sh_table16(const double *A, const double *B, const int *W) {
 #endif
 }
 
+// x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
+// offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
+// relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
 struct RedLog {
   int e, i;
   double m;
 };
-// `i` is the raw bin index: the register-table shuffle reads lane i mod 32,
-// which holds entry i mod 16 (the table is replicated in both half-warps), so
-// the fast path needs no mask; direct table reads use i & 15.
+// `i` is the raw bin index (bits above the 16-bin field included): table
+// reads use i & 15.
 CR_F RedLog red_log(double xd) {
   int h = d2hi(xd);
   int hh = h - 0x3FE88000;
@@ -732,8 +732,7 @@ struct FnTrig {
   CR_F static bool in_main(uint32_t xb) {
     return in_range(xb << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u);
   }
-  // sin and cos from one reduction with one set of table shuffles (shuffles
-  // are not common-subexpression eliminated, so sincosf must share them).
+  // sin and cos from one reduction and one table read.
   CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
