@@ -30,8 +30,10 @@
  *   - host-pointer calls are synchronous; _dev calls take device pointers
  *     and a cudaStream_t (passed as void*, NULL = default stream) and are
  *     stream-ordered; in-place (x == y) is allowed; any alignment accepted.
- *   - reentrant: the library keeps only a mutex-guarded staging workspace for
- *     the host-pointer calls and device-side counters.
+ *   - reentrant: the library keeps per device a mutex-guarded staging
+ *     workspace for the host-pointer calls (see crvec_workspace_bytes) and
+ *     device-side counters; host-pointer calls on one device are serialised,
+ *     calls on different devices run concurrently; _dev calls take no lock.
  */
 #ifndef CRVEC_H
 #define CRVEC_H
@@ -133,6 +135,22 @@ int crvec_log_dev(const double *x, double *y, size_t n, crvec_mode_t mode, void 
 int crvec_f64_accurate_dev(int fn, const double *x, double *y, size_t n, crvec_mode_t mode,
                            void *stream);
 
+/* Host-pointer callout: every lane through the binary64 accurate path (fn 0 =
+ * exp2, 1 = log). Replaces the reference's scalar MPFR fallback
+ * callout(FuncId, double, RoundingMode) (ref: proj/include/crvec/kernels_f64.hpp:58-59,
+ * proj/src/kernels_f64.cpp:78-80). */
+int crvec_callout_f64(int fn, const double *x, double *y, size_t n, crvec_mode_t mode);
+
+/* The reference's Ziv straddle test over n lanes (ref: proj/include/crvec/kernels_f64.hpp:27-56,
+ * proj/src/kernels_f64.cpp:63-76 round_test_lane): per lane, bound
+ * b = (eps_rel[i] |hi[i]| + eps_abs[i]) (1 + 2^-30) + 2^-1000; value[i] = (hi + lo - b) * 2^scale[i]
+ * rounded exactly to binary64 in `mode` (normal, subnormal or overflowing);
+ * decided[i] = 1 iff (hi + lo + b) * 2^scale[i] rounds to the same value.
+ * scale / eps_rel / eps_abs may be NULL (all zero). Host pointers; evaluated on the GPU. */
+int crvec_round_test_f64(const double *hi, const double *lo, const int64_t *scale,
+                         const double *eps_rel, const double *eps_abs, crvec_mode_t mode,
+                         double *value, unsigned char *decided, size_t n);
+
 /* ---- exhaustive binary32 sweep (verify) ----
  * For chunks [chunk_lo, chunk_hi) of 2^20 bit patterns (chunk c = patterns
  * c<<20 .. (c<<20)+2^20-1), adds into hashes[(c - chunk_lo)*4 + mode]
@@ -155,6 +173,22 @@ int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_
 int crvec_hardcase_scan_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, double rel_threshold,
                             uint32_t *out_bits, double *out_dist, uint64_t capacity,
                             uint64_t *count, void *stream);
+
+/* ---- host-path workspace ----
+ * The host-pointer calls stage data through per-device device buffers
+ * (4 pipeline slots x {input, output[, second output for sincosf]} x up to
+ * 64 MiB), allocated on first use and kept for later calls. */
+int crvec_workspace_release(void);    /* free the current device's staging buffers */
+size_t crvec_workspace_bytes(void);   /* bytes currently held on the current device */
+
+/* Binary64 hard-case screen: for the n inputs x (device), the fast-path value
+ * of exp2 (fn 0) or log (fn 1) and its distance to the nearest binary64 rounding
+ * boundary relative to the value; main-range inputs closer than rel_threshold
+ * are appended to out_x / out_dist (device, capacity entries), *count (device,
+ * caller-zeroed) = candidates found. Seeds the binary64 hard set whose exact
+ * ranking uses the reference's boundary_distance_f64 (ref: proj/src/oracle.cpp:502-563). */
+int crvec_hardcase_scan_f64(int fn, const double *x, size_t n, double rel_threshold, double *out_x,
+                            double *out_dist, uint64_t capacity, uint64_t *count, void *stream);
 
 /* ---- accounting / errors ---- */
 int crvec_stats_get(crvec_stats_t *out);   /* cumulative since load / last reset */

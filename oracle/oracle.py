@@ -20,6 +20,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcrvec_oracle.so")
 REF_PATH = os.path.join(HERE, "_ref", "libcrvec_ref.so")
+# the reference's own kernels (AVX-512 build and an x86-64-v2 build)
+REFK_PATHS = (os.path.join(HERE, "_ref", "libcrvec_refk.so"), os.path.join(HERE, "_ref", "libcrvec_refk_v2.so"))
 
 # Oracle function ids (first three = reference FuncId order,
 # ref: proj/include/crvec/oracle.hpp:21).
@@ -35,6 +37,7 @@ _u32p = ctypes.POINTER(ctypes.c_uint32)
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _lib = None
 _ref = None
+_refk = None
 
 
 def build(ref: bool = True) -> None:
@@ -98,6 +101,69 @@ def ref():
                                           ctypes.c_int]
         _ref = R
     return _ref
+
+
+def _host_has_avx512() -> bool:
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+    return all(f in flags for f in ("avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"))
+
+
+def refk_path() -> str | None:
+    """The reference-kernel library for this host (AVX-512 build if the host has it)."""
+    p4, p2 = REFK_PATHS
+    if _host_has_avx512() and os.path.exists(p4):
+        return p4
+    return p2 if os.path.exists(p2) else None
+
+
+def refk_available() -> bool:
+    return refk_path() is not None
+
+
+def refk():
+    """The REFERENCE's kernels (cr_exp2f/cr_log2f/cr_exp2/cr_log, round_test_lane)."""
+    global _refk
+    if _refk is None:
+        p = refk_path()
+        if p is None:
+            raise RuntimeError("reference kernels not built: make -C oracle ref")
+        K = ctypes.CDLL(p)
+        K.crvec_refk_round_test_lane.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int64,
+                                                 ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                                 ctypes.POINTER(ctypes.c_double)]
+        K.crvec_refk_f32.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        K.crvec_refk_f64.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                     ctypes.c_int, ctypes.c_int, _u64p]
+        K.crvec_refk_bounds.argtypes = [ctypes.POINTER(ctypes.c_double)]
+        _refk = K
+    return _refk
+
+
+def refk_f32(fn: str, xbits: np.ndarray, mode: int, threads: int = 0, vector: bool = True) -> np.ndarray:
+    """The reference's cr_exp2f<16> / cr_log2f<16> (Backend::vector, or the
+    per-lane Backend::reference) over an array, std::thread over chunks."""
+    x = np.ascontiguousarray(xbits, dtype=np.uint32)
+    y = np.empty_like(x)
+    rc = refk().crvec_refk_f32(FN[fn], x.ctypes.data, y.ctypes.data, x.size, int(mode), int(vector), threads)
+    if rc != 0:
+        raise RuntimeError(f"reference kernel: no binary32 {fn}")
+    return y
+
+
+def refk_f64(fn: str, xbits: np.ndarray, mode: int, threads: int = 0):
+    """The reference's cr_exp2<16> / cr_log<16> (counted); returns (y, callouts)."""
+    x = np.ascontiguousarray(xbits, dtype=np.uint64)
+    y = np.empty_like(x)
+    und = ctypes.c_uint64(0)
+    rc = refk().crvec_refk_f64(FN[fn], x.ctypes.data, y.ctypes.data, x.size, int(mode), threads,
+                               ctypes.byref(und))
+    if rc != 0:
+        raise RuntimeError(f"reference kernel: no binary64 {fn}")
+    return y, int(und.value)
 
 
 def _p32(a):

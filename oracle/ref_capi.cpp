@@ -1,6 +1,6 @@
 // TEST INFRASTRUCTURE ONLY — C entry points over the REFERENCE's own oracle,
 // compiled unmodified from /root/reference/proj/src/{fpbits,oracle}.cpp by
-// oracle/build_ref.sh into oracle/_ref/libcrvec_ref.so. Used to pin the C
+// the `ref` target of oracle/Makefile into oracle/_ref/libcrvec_ref.so. Used to pin the C
 // restatement (oracle/crvec_oracle.c) and as the reference CPU arm of bench.py.
 // ref: proj/include/crvec/oracle.hpp:74-90, proj/include/crvec/fpbits.hpp:131.
 #include <atomic>
@@ -153,6 +153,55 @@ uint64_t crvec_ref_hardest_case_search(int f, uint32_t lo, uint32_t hi, uint32_t
       out_dist[i] = v[i].scaled_distance;
     }
   return v.size();
+}
+
+// Exhaustive-sweep golden hashes straight from the reference's oracle:
+// for chunks [chunk_lo, chunk_hi) of 2^20 binary32 patterns,
+//   h[(c - chunk_lo)*4 + m] = sum_p mix64((oracle_all_modes_f32(f, p)[m] << 32) | p)
+// (the hash of include/crvec.h crvec_sweep_f32 / oracle/crvec_oracle.c).
+// oracle_all_modes_f32 is ref: proj/src/oracle.cpp:347-388, unmodified.
+// Returns the number of patterns whose oracle call threw (precision cap).
+static inline uint64_t ref_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
+uint64_t crvec_ref_sweep_hashes(int f, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t* h,
+                                int threads) {
+  if (threads <= 0) threads = static_cast<int>(std::thread::hardware_concurrency());
+  if (threads <= 0) threads = 1;
+  const uint32_t nchunks = chunk_hi - chunk_lo;
+  std::atomic<uint32_t> next{0};
+  std::atomic<uint64_t> fails{0};
+  auto work = [&]() {
+    for (;;) {
+      const uint32_t i = next.fetch_add(1);
+      if (i >= nchunks) break;
+      const uint32_t c = chunk_lo + i;
+      uint64_t acc[4] = {0, 0, 0, 0};
+      for (uint32_t k = 0; k < (1u << 20); ++k) {
+        const uint32_t p = (c << 20) | k;
+        uint32_t o[4] = {0x7FC00000u, 0x7FC00000u, 0x7FC00000u, 0x7FC00000u};
+        try {
+          auto r = oracle_all_modes_f32(static_cast<FuncId>(f), Binary32(p));
+          for (int m = 0; m < 4; ++m) o[m] = r.value[m].bits;
+        } catch (...) {
+          fails.fetch_add(1);
+        }
+        for (int m = 0; m < 4; ++m) acc[m] += ref_mix64((static_cast<uint64_t>(o[m]) << 32) | p);
+      }
+      std::memcpy(h + 4ull * i, acc, sizeof(acc));
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 1; t < threads; ++t) ts.emplace_back(work);
+  work();
+  for (auto& t : ts) t.join();
+  return fails.load();
 }
 
 }  // extern "C"

@@ -117,6 +117,22 @@ def _stream_ptr(t):
     return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
 
+def _check_out(t, ref, what):
+    """A caller-supplied output tensor must match the input: same CUDA device,
+    dtype and element count, and contiguous (the kernels write numel() elements
+    through the raw pointer)."""
+    if (not _is_torch(t) or t.device != ref.device or t.dtype != ref.dtype
+            or t.numel() != ref.numel() or not t.is_contiguous()):
+        raise CrvecError(f"{what} must be a contiguous {ref.dtype} tensor on {ref.device} "
+                         f"with {ref.numel()} elements")
+
+
+def _check_out_np(a, ref, what):
+    if (not isinstance(a, np.ndarray) or a.dtype != ref.dtype or a.size != ref.size
+            or not a.flags.c_contiguous or not a.flags.writeable):
+        raise CrvecError(f"{what} must be a writeable contiguous {ref.dtype} array of {ref.size} elements")
+
+
 def eval_f32(name: str, x, mode: int = RoundingMode.NearestEven, out=None, out2=None):
     """Evaluate binary32 function `name` elementwise; returns out (and out2 for sincosf)."""
     fn = FN_IDS[name]
@@ -127,16 +143,22 @@ def eval_f32(name: str, x, mode: int = RoundingMode.NearestEven, out=None, out2=
             raise CrvecError("torch input must be a CUDA float32 tensor")
         x = x.contiguous()
         out = torch.empty_like(x) if out is None else out
-        if fn == FN_IDS["sincosf"] and out2 is None:
-            out2 = torch.empty_like(x)
-        _check(L.crvec_eval_f32_dev(fn, x.data_ptr(), out.data_ptr(),
-                                    out2.data_ptr() if out2 is not None else None,
-                                    x.numel(), int(mode), _stream_ptr(x)))
+        _check_out(out, x, "out")
+        if fn == FN_IDS["sincosf"]:
+            out2 = torch.empty_like(x) if out2 is None else out2
+            _check_out(out2, x, "out2")
+        # the C ABI launches on the current device: make it the tensor's
+        with torch.cuda.device(x.device):
+            _check(L.crvec_eval_f32_dev(fn, x.data_ptr(), out.data_ptr(),
+                                        out2.data_ptr() if out2 is not None else None,
+                                        x.numel(), int(mode), _stream_ptr(x)))
     else:
         x = np.ascontiguousarray(x, dtype=np.float32)
         out = np.empty_like(x) if out is None else out
-        if fn == FN_IDS["sincosf"] and out2 is None:
-            out2 = np.empty_like(x)
+        _check_out_np(out, x, "out")
+        if fn == FN_IDS["sincosf"]:
+            out2 = np.empty_like(x) if out2 is None else out2
+            _check_out_np(out2, x, "out2")
         _check(L.crvec_eval_f32(fn, x.ctypes.data, out.ctypes.data,
                                 out2.ctypes.data if out2 is not None else None, x.size, int(mode)))
     return (out, out2) if fn == FN_IDS["sincosf"] else out
@@ -169,10 +191,27 @@ def _f64(name, x, mode, stats: FastPathStats | None):
         raise CrvecError("binary64 kernels not built")
     if _is_torch(x):
         import torch
+        if not x.is_cuda or x.dtype != torch.float64:
+            raise CrvecError("torch input must be a CUDA float64 tensor")
         x = x.contiguous()
         out = torch.empty_like(x)
-        _check(getattr(L, f"crvec_{name}_dev")(x.data_ptr(), out.data_ptr(), x.numel(), int(mode),
-                                               _stream_ptr(x)))
+        if stats is None:
+            with torch.cuda.device(x.device):
+                _check(getattr(L, f"crvec_{name}_dev")(x.data_ptr(), out.data_ptr(), x.numel(),
+                                                       int(mode), _stream_ptr(x)))
+            return out
+        # counted form: the device counters around a stream-ordered call
+        with torch.cuda.device(x.device):
+            torch.cuda.current_stream(x.device).synchronize()
+            before = _read_stats()
+            _check(getattr(L, f"crvec_{name}_dev")(x.data_ptr(), out.data_ptr(), x.numel(),
+                                                   int(mode), _stream_ptr(x)))
+            torch.cuda.current_stream(x.device).synchronize()
+            after = _read_stats()
+        stats.lanes += x.numel()
+        stats.undecided += after.fast_undecided - before.fast_undecided
+        stats.accurate_undecided += after.accurate_undecided - before.accurate_undecided
+        stats.host_callouts += after.host_callouts - before.host_callouts
         return out
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.empty_like(x)
@@ -217,23 +256,29 @@ def sweep_f32(name: str, chunk_lo: int = 0, chunk_hi: int = 4096, force_accurate
 
     Returns (hashes[chunks, 4] uint64, hashes_cos or None, accurate_lanes)."""
     import torch
-    dev = torch.device("cuda") if device is None else device
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     n = chunk_hi - chunk_lo
     h = torch.zeros((n, 4), dtype=torch.int64, device=dev)
     h2 = torch.zeros((n, 4), dtype=torch.int64, device=dev) if name == "sincosf" else None
     ctr = torch.zeros(4, dtype=torch.int64, device=dev)
-    _check(lib().crvec_sweep_f32(FN_IDS[name], chunk_lo, chunk_hi, h.data_ptr(),
-                                 h2.data_ptr() if h2 is not None else None, ctr.data_ptr(),
-                                 int(force_accurate), _stream_ptr(h)))
+    with torch.cuda.device(dev):
+        _check(lib().crvec_sweep_f32(FN_IDS[name], chunk_lo, chunk_hi, h.data_ptr(),
+                                     h2.data_ptr() if h2 is not None else None, ctr.data_ptr(),
+                                     int(force_accurate), _stream_ptr(h)))
     torch.cuda.current_stream(dev).synchronize()
     to_np = lambda t: t.cpu().numpy().view(np.uint64)  # noqa: E731
     return to_np(h), (to_np(h2) if h2 is not None else None), int(ctr[0].item())
 
 
-def stats() -> Stats:
+def _read_stats() -> Stats:
     st = Stats()
     _check(lib().crvec_stats_get(ctypes.byref(st)))
     return st
+
+
+def stats() -> Stats:
+    """Cumulative counters of the current device (crvec_stats_get)."""
+    return _read_stats()
 
 
 def reset_stats() -> None:

@@ -22,6 +22,11 @@ int f64_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStr
                  unsigned long long *ctr);
 int f64_accurate_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
                           unsigned long long *ctr);
+int hardscan64_dispatch(int fn, const double *x, size_t n, double thr, double *ox, double *od,
+                        unsigned long long cap, unsigned long long *count, cudaStream_t s);
+int round_test_dispatch(const double *hi, const double *lo, const long long *scale,
+                        const double *eps_rel, const double *eps_abs, int mode, double *val,
+                        unsigned char *decided, size_t n, cudaStream_t s);
 }  // namespace crvec
 
 using namespace crvec;
@@ -29,22 +34,25 @@ using namespace crvec;
 namespace {
 
 constexpr int kMaxDev = 16;
-constexpr size_t kChunk = size_t(1) << 24;  // host path pipeline chunk (elements, measured: 2^21 10.3, 2^22 11.1, 2^24 11.4 Gelem/s)
-constexpr int kPipe = 4;                     // host path streams / staging sets
+// Host-path pipeline chunk: 64 MiB of input per chunk (2^24 binary32 or 2^23
+// binary64 elements; measured binary32: 2^21 10.3, 2^22 11.1, 2^24 11.4 Gelem/s).
+constexpr size_t kChunkBytes = size_t(64) << 20;
+constexpr int kPipe = 4;  // host path streams / staging sets
 
 FnEntry g_table[CRVEC_FN_COUNT];
 std::once_flag g_table_once;
-std::mutex g_mu;
 std::atomic<uint64_t> g_lanes{0};
 thread_local char g_err[256] = "";
 
 struct Dev {
-  bool init = false;
+  std::atomic<bool> init{false};
+  std::mutex mu;  // guards initialisation and this device's host-path staging
   int status = CRVEC_ENODEV;
   unsigned long long *counters = nullptr;  // [0] lanes (unused), [1] fast_undecided, [2] acc, [3] host
-  // host-path staging
+  // host-path staging: x, y and (sincosf only) the second output per pipe slot
   void *buf[kPipe][3] = {};
   size_t buf_bytes = 0;
+  bool buf_y2 = false;
   cudaStream_t st[kPipe] = {};
 };
 Dev g_dev[kMaxDev];
@@ -54,7 +62,8 @@ int cuda_fail(cudaError_t e) {
   return e == cudaErrorMemoryAllocation ? CRVEC_ENOMEM : CRVEC_ECUDA;
 }
 
-// Current device, initialised on first use (sm_100 required).
+// Current device, initialised on first use (sm_100 required). Each device's
+// state is initialised once under its own mutex (double-checked on an atomic).
 int device(Dev **out) {
   std::call_once(g_table_once, [] {
     register_exp(g_table);
@@ -70,9 +79,9 @@ int device(Dev **out) {
     return CRVEC_ENODEV;
   }
   Dev &D = g_dev[d];
-  if (!D.init) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!D.init) {
+  if (!D.init.load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(D.mu);
+    if (!D.init.load(std::memory_order_relaxed)) {
       cudaDeviceProp p;
       e = cudaGetDeviceProperties(&p, d);
       if (e != cudaSuccess || p.major != 10) {
@@ -85,7 +94,7 @@ int device(Dev **out) {
       } else {
         D.status = CRVEC_OK;
       }
-      D.init = true;
+      D.init.store(true, std::memory_order_release);
     }
   }
   *out = &D;
@@ -107,16 +116,25 @@ int launch(Dev *D, int fn, const float *x, float *y, float *y2, size_t n, int mo
   return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
 }
 
-int ensure_staging(Dev *D, size_t bytes) {
-  if (D->buf_bytes >= bytes) return CRVEC_OK;
+void free_staging(Dev *D) {
   for (auto &b : D->buf)
     for (auto &p : b)
       if (p) { cudaFree(p); p = nullptr; }
   D->buf_bytes = 0;
+  D->buf_y2 = false;
+}
+
+// Staging for the host path (caller holds D->mu): per pipe slot an input and
+// an output buffer of `bytes`, plus a second output for sincosf.
+int ensure_staging(Dev *D, size_t bytes, bool y2) {
+  if (D->buf_bytes >= bytes && (D->buf_y2 || !y2)) return CRVEC_OK;
+  if (D->buf_bytes < bytes) bytes = bytes > D->buf_bytes ? bytes : D->buf_bytes;
+  y2 = y2 || D->buf_y2;
+  free_staging(D);
   for (auto &b : D->buf)
-    for (auto &p : b) {
-      cudaError_t e = cudaMalloc(&p, bytes);
-      if (e != cudaSuccess) return cuda_fail(e);
+    for (int j = 0; j < (y2 ? 3 : 2); ++j) {
+      cudaError_t e = cudaMalloc(&b[j], bytes);
+      if (e != cudaSuccess) { free_staging(D); return cuda_fail(e); }
     }
   for (auto &s : D->st)
     if (!s) {
@@ -124,6 +142,7 @@ int ensure_staging(Dev *D, size_t bytes) {
       if (e != cudaSuccess) return cuda_fail(e);
     }
   D->buf_bytes = bytes;
+  D->buf_y2 = y2;
   return CRVEC_OK;
 }
 
@@ -131,11 +150,14 @@ int ensure_staging(Dev *D, size_t bytes) {
 // staging buffers) so H2D copies, kernels and D2H copies of different chunks
 // overlap and both copy engines stay busy (fully when the host buffers are
 // pinned; with two streams an H2D would wait behind its stream's D2H).
+// Serialised per device (the staging is per device); calls on different
+// devices run concurrently.
 template <class T, class Launch>
 int host_pipeline(Dev *D, const T *x, T *y, T *y2, size_t n, Launch &&lf) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(D->mu);
+  const size_t kChunk = kChunkBytes / sizeof(T);
   size_t chunk = n < kChunk ? n : kChunk;
-  int rc = ensure_staging(D, chunk * sizeof(T));
+  int rc = ensure_staging(D, chunk * sizeof(T), y2 != nullptr);
   if (rc) return rc;
   size_t i = 0;
   for (size_t off = 0; off < n; off += chunk, ++i) {
@@ -273,6 +295,70 @@ int crvec_f64_accurate_dev(int fn, const double *x, double *y, size_t n, crvec_m
                                                                                        : CRVEC_OK;
 }
 
+int crvec_hardcase_scan_f64(int fn, const double *x, size_t n, double rel_threshold, double *out_x,
+                            double *out_dist, uint64_t capacity, uint64_t *count, void *stream) {
+  if (fn < 0 || fn > 1 || !count || (n && !x) || (capacity && (!out_x || !out_dist))) return CRVEC_EINVAL;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  return hardscan64_dispatch(fn, x, n, rel_threshold, out_x, out_dist, (unsigned long long)capacity,
+                             (unsigned long long *)count, (cudaStream_t)stream)
+             ? CRVEC_ECUDA : CRVEC_OK;
+}
+
+// Host-pointer callout: every lane through the binary64 accurate path (the
+// GPU replacement of the reference's scalar MPFR callout).
+int crvec_callout_f64(int fn, const double *x, double *y, size_t n, crvec_mode_t m) {
+  if (fn < 0 || fn > 1 || m < 0 || m > 3 || (n && (!x || !y))) return CRVEC_EINVAL;
+  if (!n) return CRVEC_OK;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  return host_pipeline<double>(D, x, y, nullptr, n,
+                               [&](const double *dx, double *dy, double *, size_t cnt, cudaStream_t s) {
+                                 return f64_accurate_dispatch(fn, dx, dy, cnt, m, s, D->counters + 1)
+                                            ? CRVEC_ECUDA : CRVEC_OK;
+                               });
+}
+
+int crvec_round_test_f64(const double *hi, const double *lo, const int64_t *scale,
+                         const double *eps_rel, const double *eps_abs, crvec_mode_t m, double *value,
+                         unsigned char *decided, size_t n) {
+  if (m < 0 || m > 3 || (n && (!hi || !lo || !value || !decided))) return CRVEC_EINVAL;
+  if (!n) return CRVEC_OK;
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  // one device block: hi, lo, value, scale, eps_rel, eps_abs (8 B each), decided (1 B)
+  const size_t b8 = n * 8;
+  char *buf = nullptr;
+  e = cudaMallocAsync((void **)&buf, 6 * b8 + n, s);
+  if (e == cudaSuccess) {
+    double *dh = (double *)buf, *dl = dh + n, *dv = dl + n;
+    long long *dsc = scale ? (long long *)(dv + n) : nullptr;
+    double *der = eps_rel ? dv + 2 * n : nullptr, *dea = eps_abs ? dv + 3 * n : nullptr;
+    unsigned char *dd = (unsigned char *)(dv + 4 * n);
+    auto h2d = [&](void *d, const void *h) {
+      return h ? cudaMemcpyAsync(d, h, b8, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    };
+    if ((e = h2d(dh, hi)) == cudaSuccess && (e = h2d(dl, lo)) == cudaSuccess &&
+        (e = h2d(dsc, scale)) == cudaSuccess && (e = h2d(der, eps_rel)) == cudaSuccess &&
+        (e = h2d(dea, eps_abs)) == cudaSuccess) {
+      if (round_test_dispatch(dh, dl, dsc, der, dea, m, dv, dd, n, s)) e = cudaGetLastError();
+      if (e == cudaSuccess && (e = cudaMemcpyAsync(value, dv, b8, cudaMemcpyDeviceToHost, s)) == cudaSuccess)
+        e = cudaMemcpyAsync(decided, dd, n, cudaMemcpyDeviceToHost, s);
+    }
+    cudaFreeAsync(buf, s);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e == cudaSuccess) e = e2;
+  return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
 #endif
 
 // ---- sweep ----
@@ -303,6 +389,24 @@ int crvec_hardcase_scan_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi,
                                    (unsigned long long)capacity, (unsigned long long *)count,
                                    (cudaStream_t)stream);
   return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+}
+
+// ---- workspace ----
+int crvec_workspace_release(void) {
+  Dev *D;
+  int rc = device(&D);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(D->mu);
+  for (auto s : D->st)
+    if (s) cudaStreamSynchronize(s);
+  free_staging(D);
+  return CRVEC_OK;
+}
+size_t crvec_workspace_bytes(void) {
+  Dev *D;
+  if (device(&D)) return 0;
+  std::lock_guard<std::mutex> lk(D->mu);
+  return D->buf_bytes * kPipe * (D->buf_y2 ? 3 : 2);
 }
 
 // ---- accounting ----

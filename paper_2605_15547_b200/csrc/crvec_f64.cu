@@ -278,6 +278,180 @@ int f64_accurate_dispatch(int fn, const double *x, double *y, size_t n, int mode
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+// ------------------------------------------------------ hard-case screen ----
+// Binary64 worst-case screen: the fast-path value
+// of every input's main-range evaluation and its distance to the nearest
+// binary64 rounding boundary (representable value or midpoint, any mode),
+// relative to the value; inputs closer than `thr` are appended. The ranking is
+// then confirmed with the reference's boundary_distance_f64 (MPFR).
+__device__ __forceinline__ double boundary_rel_distance64(DD v) {
+  const double h = v.hi;
+  if (!(dabs(h) < INFINITY) || h == 0.0) return 1.0;
+  const uint64_t hb = d2u(dabs(h));
+  // h itself is a boundary; the next ones on the side of lo are h +- ulp/2,
+  // or ulp/4 below a power of two (the binade below is twice as dense)
+  double half = u2d(hb & 0x7FF0000000000000ull) * 0x1p-53;
+  if ((hb & 0xFFFFFFFFFFFFFull) == 0 && (v.lo < 0.0) == (h > 0.0)) half *= 0.5;
+  const double al = dabs(v.lo);
+  return fmin(al, dabs(half - al)) / dabs(h);
+}
+
+template <int FN>
+__global__ void __launch_bounds__(kT64) k_hardscan64(const double *x, uint64_t n, double thr,
+                                                     double *ox, double *od, unsigned long long cap,
+                                                     unsigned long long *count) {
+  __shared__ F64Tab T;
+  load_tables<FN>(T);
+  for (uint64_t i = (uint64_t)blockIdx.x * kT64 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kT64) {
+    const double xv = x[i];
+    bool main;
+    DD V;
+    if (FN == 0) {
+      main = exp2d_main(xv) && xv < 1024.0 && xv >= -1022.0 && xv != floor(xv);
+      V = exp2d_value(main ? xv : 0.5, T).V;
+    } else {
+      const uint64_t xb = d2u(xv);
+      main = xb - 0x0010000000000000ull < 0x7FE0000000000000ull && xv != 1.0;
+      V = logd_value(main ? xv : 2.0, 0, T);
+    }
+    if (main) {
+      const double d = boundary_rel_distance64(V);
+      if (d < thr) {
+        const unsigned long long k = atomicAdd(count, 1ull);
+        if (k < cap) {
+          ox[k] = xv;
+          od[k] = d;
+        }
+      }
+    }
+  }
+}
+
+int hardscan64_dispatch(int fn, const double *x, size_t n, double thr, double *ox, double *od,
+                        unsigned long long cap, unsigned long long *count, cudaStream_t s) {
+  if (fn < 0 || fn > 1) return -1;
+  if (!n) return 0;
+  uint64_t blocks = (n + kT64 - 1) / kT64;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  if (fn == 0) k_hardscan64<0><<<(unsigned)blocks, kT64, 0, s>>>(x, n, thr, ox, od, cap, count);
+  else k_hardscan64<1><<<(unsigned)blocks, kT64, 0, s>>>(x, n, thr, ox, od, cap, count);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// ------------------------------------------------- reference round test ----
+// The reference's Ziv straddle test as a standalone batch operation
+// (ref: proj/src/kernels_f64.cpp:63-76 round_test_lane, kernels_f64.hpp:27-56):
+// bound b = RN(RN(eps_rel |hi| + eps_abs) (1 + 2^-30) + 2^-1000), the two ends
+// fast_two_sum(hi, lo -+ b) are rounded EXACTLY after scaling by 2^scale
+// (normal, subnormal and overflowing results alike) in the requested mode,
+// and the lane is decided iff both ends round to the same binary64. The kernels
+// use the cheaper in-register form round_test64() (no scale, b precomputed);
+// this one serves the C++ compatibility surface (round_test<W>).
+
+// Round sign * mant * 2^(E - 63) (mant bit 63 set; `sticky`: nonzero bits
+// below mant) to binary64 in mode M, subnormals and overflow included.
+template <int M>
+__device__ __forceinline__ double round_parts64(bool neg, int E, uint64_t mant, bool sticky) {
+  const uint64_t sgn = neg ? 0x8000000000000000ull : 0ull;
+  const bool to_inf = M == RNE || (M == RU && !neg) || (M == RD && neg);
+  if (E > 1023) return u2d(sgn | (to_inf ? 0x7FF0000000000000ull : 0x7FEFFFFFFFFFFFFFull));
+  const int sh = E >= -1022 ? 11 : 11 + (-1022 - E);  // bits dropped below the kept significand
+  uint64_t kept;
+  bool rb, st;
+  if (sh >= 65) {
+    kept = 0; rb = false; st = sticky || mant != 0;
+  } else if (sh == 64) {
+    kept = 0; rb = (mant >> 63) != 0; st = sticky || (mant << 1) != 0;
+  } else {
+    kept = mant >> sh;
+    rb = ((mant >> (sh - 1)) & 1u) != 0;
+    st = sticky || (mant & ((1ull << (sh - 1)) - 1u)) != 0;
+  }
+  const bool inexact = rb || st;
+  bool up;
+  if (M == RNE) up = rb && (st || (kept & 1u));
+  else if (M == RZ) up = false;
+  else if (M == RU) up = !neg && inexact;
+  else up = neg && inexact;
+  kept += up ? 1u : 0u;
+  if (E >= -1022) {
+    if (kept >> 53) { kept >>= 1; ++E; }
+    if (E > 1023) return u2d(sgn | (to_inf ? 0x7FF0000000000000ull : 0x7FEFFFFFFFFFFFFFull));
+    return u2d(sgn | ((uint64_t)(E + 1023) << 52) | (kept & 0xFFFFFFFFFFFFFull));
+  }
+  return u2d(sgn | kept);  // subnormal (a carry to 2^52 encodes the least normal)
+}
+
+// Exact rounding of (s + e) * 2^n, s normal, |e| <= ulp(s)/2: s's significand
+// in a 72-bit window (19 guard bits), e added in guard-lsb units; the bits of
+// e below the window only set the sticky flag.
+template <int M>
+__device__ __forceinline__ double round_pair_scaled(double s, double e, long long n) {
+  const uint64_t bs = d2u(s);
+  const bool neg = (bs >> 63) != 0;
+  const int es = (int)((bs >> 52) & 0x7FF) - 1023;
+  const unsigned __int128 M53 = (bs & 0xFFFFFFFFFFFFFull) | 0x10000000000000ull;
+  unsigned __int128 m = M53 << 19;  // value = m * 2^(es - 71)
+  bool sticky = false;
+  if (e != 0.0) {
+    const double w = ldexp(e, 71 - es);  // exact: e's bits above 2^(es-71)
+    const double aw = fabs(w);
+    const uint64_t whole = (uint64_t)aw;
+    const bool frac = aw != (double)whole;
+    if ((e < 0.0) != neg) {
+      m -= whole;
+      m -= frac ? 1u : 0u;
+    } else {
+      m += whole;
+    }
+    sticky = frac;
+  }
+  const uint64_t hi = (uint64_t)(m >> 64), lo = (uint64_t)m;
+  const int msb = hi ? 64 + 63 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+  const int drop = msb - 63;
+  uint64_t mant;
+  if (drop > 0) {
+    sticky = sticky || (lo & ((1ull << drop) - 1u)) != 0;
+    mant = (uint64_t)(m >> drop);
+  } else {
+    mant = lo << (-drop);
+  }
+  const long long E = (long long)es - 71 + msb + n;
+  const int Ec = E > 2000 ? 2000 : (E < -2000 ? -2000 : (int)E);
+  return round_parts64<M>(neg, Ec, mant, sticky);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kT64) k_round_test(const double *hi, const double *lo,
+                                                     const long long *scale, const double *eps_rel,
+                                                     const double *eps_abs, double *val,
+                                                     unsigned char *decided, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * kT64 + threadIdx.x;
+  if (i >= n) return;
+  const double h = hi[i], l = lo[i];
+  const long long sc = scale ? scale[i] : 0;
+  double b = fma_(eps_rel ? eps_rel[i] : 0.0, dabs(h), eps_abs ? eps_abs[i] : 0.0);
+  b = add_(mul_(b, 1.0 + 0x1p-30), 0x1p-1000);  // absorb the bound's own rounding
+  const DD le = fast_two_sum(h, sub_(l, b)), he = fast_two_sum(h, add_(l, b));
+  const double rl = round_pair_scaled<M>(le.hi, le.lo, sc);
+  const double rh = round_pair_scaled<M>(he.hi, he.lo, sc);
+  val[i] = rl;
+  decided[i] = d2u(rl) == d2u(rh);
+}
+
+int round_test_dispatch(const double *hi, const double *lo, const long long *scale,
+                        const double *eps_rel, const double *eps_abs, int mode, double *val,
+                        unsigned char *decided, size_t n, cudaStream_t s) {
+  using K = void (*)(const double *, const double *, const long long *, const double *, const double *,
+                     double *, unsigned char *, uint64_t);
+  static const K tab[4] = {k_round_test<RNE>, k_round_test<RZ>, k_round_test<RU>, k_round_test<RD>};
+  if (mode < 0 || mode > 3) return -1;
+  if (!n) return 0;
+  tab[mode]<<<(unsigned)((n + kT64 - 1) / kT64), kT64, 0, s>>>(hi, lo, scale, eps_rel, eps_abs, val,
+                                                              decided, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 // ctr: [1] fast_undecided, [2] accurate_undecided (device counters of the API)
 int f64_dispatch(int fn, const double *x, double *y, size_t n, int mode, cudaStream_t s,
                  unsigned long long *ctr) {

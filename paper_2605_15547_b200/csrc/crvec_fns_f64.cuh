@@ -1,11 +1,13 @@
 // Correctly rounded binary64 exp2 and log (the two double-precision functions
 // of SPEC.md, ref: PAPER.md II.B, proj/src/kernels_f64.cpp:234-307).
 //
-//  fast path   the paper's algorithms in double-double: exp2 via
-//              x = N + (i1*256 + i2*16 + i3)/4096 + R and three 16-entry DD
-//              tables (ref: kernels_f64.cpp:82-100,135-150); log via a
-//              7-bit reciprocal, a 128-entry -log(rcp) DD table and a
-//              log1p(r) series (ref: kernels_f64.cpp:102-124).
+//  fast path   the paper's algorithms, restructured for the GPU: exp2 via
+//              x = N + (64 ia + ib)/4096 + R and two 64-entry DD tables in
+//              shared memory (one DD product instead of the reference's two
+//              over three 16-entry tables, ref: kernels_f64.cpp:82-100,135-150);
+//              log via 512 bins with a 10-bit c_i (r = m c_i - 1 exact), a
+//              -log(c_i) table split on a 2^-40 grid, and r - r^2/2 + r^3 P(r)
+//              (the reference: 128 bins, 7-bit reciprocal, ref: kernels_f64.cpp:102-124).
 //  round test  Ziv straddle test in registers (ref: kernels_f64.cpp:63-76):
 //              the DD value +- eps|v| must round to the same binary64.
 //  accurate    lanes the test cannot decide (or whose result is subnormal)
@@ -312,8 +314,12 @@ CR_F F64Out round_test64(double h, double l, double b) {
   return {y1, y1 == y2};
 }
 
+// Fast-path error bounds (relative) used by the round test: the derivation
+// bounds the exp2 value's error below 2^-78.9 and the
+// log value's below 2^-76.3; tools/certify_f64.py re-derives both term by term
+// from the shipped tables and checks them on a dense grid against MPFR.
 constexpr double EPS_EXP2D = 0x1p-74;
-constexpr double EPS_LOGD = 0x1p-73;  // error analysis: < 2^-76
+constexpr double EPS_LOGD = 0x1p-73;
 
 // Lanes outside exp2's main range: NaN, +-Inf, overflow / underflow classes,
 // |x| <= 2^-55 (2^x in the gap beside 1) — all decided by rules.
@@ -339,58 +345,22 @@ CR_F bool exp2d_main(double x) {
 // 2^x = 2^N T (1 + p) with T = 2^(ia/64) 2^(ib/4096) (two 64-entry DD tables
 // in shared memory; one product instead of the paper's two over 3 x 16
 // entries, ref: proj/src/kernels_f64.cpp:82-90) and 2^R = 1 + ph + pl,
-// ph = RN(R ln2_hi). Error < 2^-74 relative before the round test; the 2^N
-// scale is an integer add to the exponent field (subnormal results take the
-// accurate path).
-template <int M>
-CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
-  if (!exp2d_main(x) || x >= 1024.0) return {exp2d_special<M>(x), true};
-  double t = fma_(x, 4096.0, SHIFTER);
-  double kd = sub_(t, SHIFTER);
-  int k = (int)d2lo(t);
-  double R = fma_(kd, -0x1p-12, x);  // exact, |R| <= 2^-13
-  int N = k >> 12, ia = (k >> 6) & 63, ib = k & 63;
-  if (R == 0.0 && (k & 4095) == 0) {  // integer x: 2^x exact (normal or subnormal)
-    double p = N >= -1022 ? u2d((uint64_t)(N + 1023) << 52) : u2d(1ull << (N + 1074));
-    return {p, true};
-  }
-  // T = A B as an unnormalised DD (|Tl| < 2^-51 |Th|)
-  const Pair64 A = T.ta[ia], B = T.tb[ib];
-  const double ah = A.a, alo = A.b, bh = B.a, blo = B.b;
-  double Th = mul_(ah, bh);
-  double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
-  double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
-  DD lin = two_prod(R, LN2D_H);
-  double pl = fma_(mul_(R, R), q, fma_(R, LN2D_L, lin.lo));
-  // V = T (1 + p) = Th + Th ph + [Tl + Th pl + Tl ph], Th ph exact
-  DD a = two_prod(Th, lin.hi);
-  DD v = fast_two_sum(Th, a.hi);
-  double lo = add_(add_(v.lo, a.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
-  DD V = fast_two_sum(v.hi, lo);
-  F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
-  if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
-  // y in [1, 2]: the exponent add is exact, 2 * 2^1023 correctly gives +Inf
-  r.y = hilo2d(d2hi(r.y) + (N << 20), d2lo(r.y));
-  return r;
-}
-
-// log fast path: x = 2^e m, m in [0.75, 1.5), 512 bins (the paper's 128,
-// ref: proj/src/kernels_f64.cpp:102-124, refined so the r^3 term needs no
-// double-double): r = m c_i - 1 exact (c_i has 10 bits, |r| < 2^-9.4),
-// log x = e ln2 - log c_i + r - r^2/2 + r^3 P(r), P of degree 6.
-// Vector-kernel form: no special-value branches. Lanes outside the normal-
-// result range, and integer x (exact 2^N), are returned undecided and resolved
-// by the warp's side-queue drain, which runs exp2d_fast (rules) first.
-template <int M>
-CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
-  const uint64_t a = d2u(x) & 0x7FFFFFFFFFFFFFFFull;
-  const bool ok = a > 0x3C80000000000000ull && x < 1024.0 && x >= -1022.0;  // 2^-55 < |x|
-  const double xs = ok ? x : 0.5;
+// ph = RN(R ln2_hi). V = T (1 + p) = Th + Th ph + [Tl + Th pl + Tl ph] with
+// Th ph exact; relative error < EPS_EXP2D before the round test (DESIGN.md
+// section 4a derives the bound); the 2^N scale is an integer add to the
+// exponent field.
+struct Exp2dV {
+  DD V;  // in [1, 2]
+  int N, k;
+  double R;
+};
+CR_F Exp2dV exp2d_value(double xs, const F64Tab &T) {
   double t = fma_(xs, 4096.0, SHIFTER);
   double kd = sub_(t, SHIFTER);
   int k = (int)d2lo(t);
   double R = fma_(kd, -0x1p-12, xs);  // exact, |R| <= 2^-13
   int N = k >> 12, ia = (k >> 6) & 63, ib = k & 63;
+  // T = A B as an unnormalised DD (|Tl| < 2^-51 |Th|)
   const Pair64 A = T.ta[ia], B = T.tb[ib];
   const double ah = A.a, alo = A.b, bh = B.a, blo = B.b;
   double Th = mul_(ah, bh);
@@ -401,15 +371,47 @@ CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
   DD aa = two_prod(Th, lin.hi);
   DD v = fast_two_sum(Th, aa.hi);
   double lo = add_(add_(v.lo, aa.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
-  DD V = fast_two_sum(v.hi, lo);
-  F64Out r = round_test64<M>(V.hi, V.lo, EPS_EXP2D * dabs(V.hi));
-  r.decided = r.decided && ok && !(R == 0.0 && (k & 4095) == 0);
-  r.y = hilo2d(d2hi(r.y) + (N << 20), d2lo(r.y));
+  return {fast_two_sum(v.hi, lo), N, k, R};
+}
+
+// Rule-complete form (scalar kernels, the side-queue drain).
+template <int M>
+CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
+  if (!exp2d_main(x) || x >= 1024.0) return {exp2d_special<M>(x), true};
+  const Exp2dV e = exp2d_value(x, T);
+  if (e.R == 0.0 && (e.k & 4095) == 0) {  // integer x: 2^x exact (normal or subnormal)
+    const int N = e.N;
+    double p = N >= -1022 ? u2d((uint64_t)(N + 1023) << 52) : u2d(1ull << (N + 1074));
+    return {p, true};
+  }
+  F64Out r = round_test64<M>(e.V.hi, e.V.lo, EPS_EXP2D * dabs(e.V.hi));
+  if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
+  // y in [1, 2]: the exponent add is exact, 2 * 2^1023 correctly gives +Inf
+  r.y = hilo2d(d2hi(r.y) + (e.N << 20), d2lo(r.y));
   return r;
 }
 
+// Vector-kernel form: no special-value branches. Lanes outside the normal-
+// result range, and integer x (exact 2^N), are returned undecided and resolved
+// by the warp's side-queue drain, which runs exp2d_fast (rules) first.
 template <int M>
-CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
+CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
+  const uint64_t a = d2u(x) & 0x7FFFFFFFFFFFFFFFull;
+  const bool ok = a > 0x3C80000000000000ull && x < 1024.0 && x >= -1022.0;  // 2^-55 < |x|
+  const Exp2dV e = exp2d_value(ok ? x : 0.5, T);
+  F64Out r = round_test64<M>(e.V.hi, e.V.lo, EPS_EXP2D * dabs(e.V.hi));
+  r.decided = r.decided && ok && !(e.R == 0.0 && (e.k & 4095) == 0);
+  r.y = hilo2d(d2hi(r.y) + (e.N << 20), d2lo(r.y));
+  return r;
+}
+
+// log fast path: x = 2^e m, m in [0.75, 1.5), 512 bins (the paper's 128,
+// ref: proj/src/kernels_f64.cpp:102-124, refined so the r^3 term needs no
+// double-double): r = m c_i - 1 exact (c_i has 10 bits, |r| < 2^-9.4),
+// log x = e ln2 - log c_i + r - r^2/2 + r^3 P(r), P of degree 6.
+// The fast-path value for a positive normal x (subnormals arrive scaled, with
+// eadj): a double-double with error below EPS_LOGD * |V|.
+CR_F DD logd_value(double xs, int eadj, const F64Tab &T) {
   int h = d2hi(xs);
   int hh = h - 0x3FE80000;
   int e = (hh >> 20) + eadj;
@@ -428,7 +430,12 @@ CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
   double tl = fma_(ed, LN2_LD, T.lll[i]);
   DD v = two_sum(th, a.hi);
   double lo = add_(add_(v.lo, tl), add_(fma_(-0.5, s.lo, a.lo), small));
-  DD V = fast_two_sum(v.hi, lo);
+  return fast_two_sum(v.hi, lo);
+}
+
+template <int M>
+CR_F F64Out logd_core(double xs, int eadj, const F64Tab &T) {
+  const DD V = logd_value(xs, eadj, T);
   return round_test64<M>(V.hi, V.lo, EPS_LOGD * dabs(V.hi));
 }
 

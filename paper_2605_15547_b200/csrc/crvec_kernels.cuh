@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "crvec_fns_f32.cuh"
 
 namespace crvec {
@@ -235,9 +237,11 @@ __device__ __forceinline__ void resolve_rare(const float (&xs)[NE], uint32_t (&y
 // and overwrites the one output float with a scalar store (same thread,
 // program order), so no scatter back into the register results is needed.
 // In-place calls are safe: the inputs are still in registers.
+// fbase (the lane's first float index) is 64-bit: a launch covers up to
+// kMaxNV vectors of VW floats, more than 2^32 floats.
 template <class F, int M, int NE, int VW>
 __device__ __forceinline__ void resolve_rare_store(const float (&xs)[NE], unsigned mask, float *yf,
-                                                   uint32_t fbase, unsigned long long *counters) {
+                                                   uint64_t fbase, unsigned long long *counters) {
   int cnt = 0;
   do {
     const unsigned low = mask & (0u - mask);
@@ -246,7 +250,7 @@ __device__ __forceinline__ void resolve_rare_store(const float (&xs)[NE], unsign
       static_assert((NE & (NE - 1)) == 0, "NE: power of two");
       // unsigned and bounded (mask has NE bits): / and % fold to shifts and masks
       const uint32_t e = ((uint32_t)__ffs(mask) - 1u) & (NE - 1u);
-      yf[fbase + 32u * VW * (e / VW) + (e % VW)] = u2f(resolve_one<F, M>(xe, cnt));
+      yf[fbase + (32u * VW * (e / VW) + (e % VW))] = u2f(resolve_one<F, M>(xe, cnt));
     }
     mask &= ~low;
   } while (__any_sync(kFull, mask != 0));
@@ -346,7 +350,7 @@ __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> 
       else mask &= ~(((1u << VW) - 1u) << (VW * k));  // stale inputs past the end
     }
     if (__any_sync(kFull, mask != 0))
-      resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, VW * base, counters);
+      resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, (uint64_t)VW * base, counters);
   } else {
     eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
 #pragma unroll
@@ -467,7 +471,7 @@ constexpr bool kSincosStore = true;
 // overwrite of the one sin or cos output a pending bit names.
 template <int M, int NE, int VW>
 __device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigned mask, float *ys,
-                                                  float *yc, uint32_t fbase,
+                                                  float *yc, uint64_t fbase,
                                                   unsigned long long *counters) {
   static_assert(NE <= 16 && (NE & (NE - 1)) == 0, "NE: power of two, <= 16 (16-bit halves)");
   int cnt = 0;
@@ -477,7 +481,7 @@ __device__ __forceinline__ void sincos_rare_store(const float (&xs)[NE], unsigne
     const float xe = gather_slot<NE>(xs, slot);
     if (low) {
       const uint32_t e = ((uint32_t)__ffs(low) - 1u) & (NE - 1u);
-      const uint32_t fi = fbase + 32u * VW * (e / VW) + (e % VW);
+      const uint64_t fi = fbase + (32u * VW * (e / VW) + (e % VW));
       if (low >> 16) yc[fi] = u2f(resolve_one<FnCos, M>(xe, cnt));
       else ys[fi] = u2f(resolve_one<FnSin, M>(xe, cnt));
     }
@@ -514,7 +518,7 @@ __device__ __forceinline__ void sincos_step(const Vec<VW> *__restrict__ x, Vec<V
     }
   }
   if (kSincosStore && __any_sync(kFull, mask != 0))
-    sincos_rare_store<M, VW * NV, VW>(xs, mask, (float *)ys, (float *)yc, VW * base, counters);
+    sincos_rare_store<M, VW * NV, VW>(xs, mask, (float *)ys, (float *)yc, (uint64_t)VW * base, counters);
 }
 
 #ifndef CRVEC_SINCOS_SHAPE
@@ -805,6 +809,18 @@ inline int max_blocks(K kernel) {
   return sms * per;
 }
 
+// Vectors per launch of the map kernels: they index vectors with 32 bits, so
+// a launch covers at most 2^31 vectors. CRVEC_SPLIT_VECTORS (read once) lowers
+// the split point so the tests can exercise multi-launch calls at small sizes.
+inline uint64_t max_vectors_per_launch() {
+  static const uint64_t v = [] {
+    const char *e = getenv("CRVEC_SPLIT_VECTORS");
+    unsigned long long k = e ? strtoull(e, nullptr, 10) : 0ull;
+    return (k >= 32 && k < (1ull << 31)) ? (uint64_t)k : (uint64_t(1) << 31);
+  }();
+  return v;
+}
+
 inline unsigned grid_for(uint64_t work_warps32, int maxb) {
   // work_warps32 = number of 32-lane slots; one warp per slot per pass
   uint64_t blocks = (work_warps32 + kWarps - 1) / kWarps;
@@ -834,7 +850,7 @@ cudaError_t launch_map(const float *x, float *y, float *, uint64_t n, cudaStream
   const float *xv = aligned ? x + head : x;
   float *yv = aligned ? y + head : y;
   // the kernel indexes vectors with 32 bits: launches of at most 2^31 vectors
-  constexpr uint64_t kMaxNV = uint64_t(1) << 31;
+  const uint64_t kMaxNV = max_vectors_per_launch();
   for (uint64_t off = 0; off < nvec; off += kMaxNV) {
     uint64_t m = nvec - off < kMaxNV ? nvec - off : kMaxNV;
     const unsigned g = grid_for((m + 32 * NV - 1) / (32 * NV), mb_vec);
@@ -866,7 +882,7 @@ cudaError_t launch_sincos(const float *x, float *ys, float *yc, uint64_t n, cuda
   const uint64_t nvec = aligned ? (n - head) / VW : 0;
   const uint64_t v0 = aligned ? head : 0;
   scalar(0, v0);
-  constexpr uint64_t kMaxNV = uint64_t(1) << 31;
+  const uint64_t kMaxNV = max_vectors_per_launch();
   for (uint64_t off = 0; off < nvec; off += kMaxNV) {
     uint64_t m = nvec - off < kMaxNV ? nvec - off : kMaxNV;
     const uint64_t f = v0 + VW * off;

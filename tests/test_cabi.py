@@ -124,3 +124,20 @@ def test_tables_at_most_16_entries_for_binary32():
         if name.endswith("Q"):
             continue  # polynomial coefficients
         assert int(n) <= 16, (name, n)
+
+
+def test_python_wrapper_rejects_host_tensors_before_the_abi(lib):
+    """Tensors must be CUDA tensors of the path's dtype: a
+    host tensor's pointer would fault the kernel, a float32 tensor in the
+    binary64 path would be written out of bounds."""
+    import torch
+    import paper_2605_15547_b200 as crvec
+    with pytest.raises(crvec.CrvecError):
+        crvec.eval_f32("logf", torch.ones(8))
+    with pytest.raises(crvec.CrvecError):
+        crvec.cr_exp2(torch.ones(8, dtype=torch.float64))
+    with pytest.raises(crvec.CrvecError):
+        crvec.cr_log(torch.ones(8, dtype=torch.float32))
+    # numpy outputs are validated too
+    with pytest.raises(crvec.CrvecError):
+        crvec.eval_f32("logf", np.ones(8, dtype=np.float32), out=np.empty(7, dtype=np.float32))

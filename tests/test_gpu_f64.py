@@ -177,3 +177,58 @@ def test_concurrent_host_callers(cuda, oracle):
         t.join()
     for i in range(6):
         assert (outs[i].view(np.uint32) == oracle.f32("log", xs[i].view(np.uint32), i % 4)).all()
+
+
+def _c5_inputs(name, seed):
+    rng = np.random.default_rng(seed)
+    if name == "exp2":
+        return np.concatenate([rng.uniform(-20, 20, 1 << 26), rng.uniform(-1075, 1024, 1 << 24),
+                               rng.integers(0, 2 ** 64, 1 << 24, dtype=np.uint64).view(np.float64)])
+    return np.concatenate([rng.uniform(0.125, 8, 1 << 26), rng.uniform(0.5, 2, 1 << 24),
+                           rng.integers(0, 2 ** 63, 1 << 24, dtype=np.uint64).view(np.float64)])
+
+
+@pytest.mark.parametrize("name", ["exp2", "log"])
+def test_config_c5_full_scale_all_modes(cuda, oracle, name):
+    """Config C5 at its stated size: 2^26 doubles on the paper's range
+    (ref: PAPER.md:194) + 2^24 wide-range + 2^24 random bit
+    patterns, all four modes, device path, bit-exact vs the oracle."""
+    x = _c5_inputs(name, 26 if name == "exp2" else 27)
+    want = oracle.f64(name, x.view(np.uint64), None)
+    xt = cuda.from_numpy(x).cuda()
+    for mode in range(4):
+        got = crvec._f64(name, xt, mode, None).cpu().numpy().view(np.uint64)
+        bad = np.nonzero(got != want[:, mode])[0]
+        assert bad.size == 0, (name, mode, bad.size, [(float(x[i]), hex(int(got[i])), hex(int(want[i, mode])))
+                                                      for i in bad[:5]])
+
+
+@pytest.mark.parametrize("name", ["exp2", "log"])
+def test_seeded_hard_set_ranked_by_reference_boundary_distance(cuda, name):
+    """Config C5 (iii): the hardest inputs of a 2^28-input GPU screen, ranked by
+    the reference's boundary_distance_f64, with the reference's own 4-mode
+    results (tools/hard_cases_f64.py -> tests/golden/hardcases_f64/). Replayed
+    (a) scattered among 2^20 random co-resident lanes on the device path, so the
+    ballot-compacted side queue sees them mixed with decided lanes, and (b)
+    through the host path."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "hardcases_f64", f"{name}.npz"))
+    hx, want = g["x"].view(np.float64), g["want"]
+    assert hx.size >= 256
+    rng = np.random.default_rng(31415)
+    lo, hi = (-20.0, 20.0) if name == "exp2" else (0.125, 8.0)
+    x = rng.uniform(lo, hi, 1 << 20)
+    pos = rng.choice(x.size, hx.size, replace=False)
+    x[pos] = hx
+    xt = cuda.from_numpy(x).cuda()
+    st = crvec.FastPathStats()
+    for mode in range(4):
+        got = crvec._f64(name, xt, mode, st if mode == 0 else None).cpu().numpy().view(np.uint64)
+        bad = np.nonzero(got[pos] != want[:, mode])[0]
+        assert bad.size == 0, (name, mode, [(float(hx[i]), hex(int(got[pos][i])), hex(int(want[i, mode])))
+                                            for i in bad[:5]])
+        goth = crvec._f64(name, hx, mode, None).view(np.uint64)
+        assert (goth == want[:, mode]).all(), (name, mode)
+    # the hardest of the set sit inside the fast path's 2^-74 window: the
+    # side queue and the accurate path are exercised
+    assert st.undecided > 0, st
