@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kT64) k_hardscan64(const double *x, uint64_t n
     } else {
       const uint64_t xb = d2u(xv);
       main = xb - 0x0010000000000000ull < 0x7FE0000000000000ull && xv != 1.0;
-      V = logd_value(main ? xv : 2.0, 0, T);
+      V = logd_value(main ? xv : 2.0, 0, T).V;
     }
     if (main) {
       const double d = boundary_rel_distance64(V);

@@ -58,11 +58,16 @@ int main() {
     CHECK(e64.lane[0] == 2.0 && e64.lane[1] == 0x1p-1074 && std::isinf(e64.lane[2]));
     CHECK(e64.lane[3] == 0x1.6a09e667f3bcdp+0);  // RU(sqrt 2)
 
-    // round test: an exactly representable value is decided in every mode;
-    // a value on a tie (RNE) with a positive bound is undecided
-    for (auto m : all_rounding_modes) {
-      RoundTestLane r = round_test_lane(DD{1.5, 0.0}, 3, 0x1p-70, 0.0, m);
-      CHECK(r.value.to_double() == 12.0);
+    // round test (the reference's semantics): the low end of the enclosure is
+    // the reported value; an exactly representable value with a positive
+    // bound is decided in RNE only (the directed modes see it straddled)
+    {
+      RoundTestLane r = round_test_lane(DD{1.5, 0.0}, 3, 0x1p-70, 0.0, RoundingMode::NearestEven);
+      CHECK(r.value.to_double() == 12.0 && r.decided);
+      r = round_test_lane(DD{1.5, 0.0}, 3, 0x1p-70, 0.0, RoundingMode::TowardZero);
+      CHECK(r.value.to_double() == std::nextafter(12.0, 0.0) && !r.decided);
+      r = round_test_lane(DD{1.5, 0x1p-60}, 3, 0x1p-70, 0.0, RoundingMode::TowardPositive);
+      CHECK(r.value.to_double() == std::nextafter(12.0, 13.0) && r.decided);
     }
     RoundTestLane tie = round_test_lane(DD{1.0, 0x1p-53}, 0, 0x1p-70, 0.0, RoundingMode::NearestEven);
     CHECK(!tie.decided);
@@ -72,7 +77,7 @@ int main() {
     v.hi.lane = {1.0, 2.0, 3.0, 1.0};
     v.lo.lane = {0.0, 0x1p-60, -0x1p-60, 0x1p-53};
     auto rt = round_test<4>(v, 0x1p-80, RoundingMode::TowardZero);
-    CHECK(rt.decided[0] && rt.decided[1] && rt.decided[2]);
+    CHECK(!rt.decided[0] && rt.decided[1] && rt.decided[2] && !rt.decided[3]);
     CHECK(rt.fast_result[1] == 2.0 && rt.fast_result[2] == std::nextafter(3.0, 0.0));
     CHECK(rt.error_bound == 0x1p-80);
 

@@ -55,7 +55,10 @@ def hard_log():
     k = np.arange(20, 53, dtype=np.float64)
     base = np.concatenate([1 + 2.0 ** -k, 1 - 2.0 ** -k, 1 + 3 * 2.0 ** -k])
     js = np.array([-1000, -100, -7, -1, 1, 5, 64, 500, 1000], dtype=np.float64)
-    return np.concatenate([base] + [base * 2.0 ** j for j in js])
+    # a round-1 fast path decided this one wrongly in RZ / RD (its fixed 2^-73
+    # bound missed the r^3-term rounding error near 1)
+    regress = np.array([1.0015369252084056])
+    return np.concatenate([base] + [base * 2.0 ** j for j in js] + [regress])
 
 
 def hard_exp2():
@@ -185,14 +188,16 @@ def _c5_inputs(name, seed):
         return np.concatenate([rng.uniform(-20, 20, 1 << 26), rng.uniform(-1075, 1024, 1 << 24),
                                rng.integers(0, 2 ** 64, 1 << 24, dtype=np.uint64).view(np.float64)])
     return np.concatenate([rng.uniform(0.125, 8, 1 << 26), rng.uniform(0.5, 2, 1 << 24),
-                           rng.integers(0, 2 ** 63, 1 << 24, dtype=np.uint64).view(np.float64)])
+                           rng.integers(0, 2 ** 63, 1 << 24, dtype=np.uint64).view(np.float64),
+                           rng.uniform(1 - 2.0 ** -9, 1 + 2.0 ** -9, 1 << 23)])  # r-dominated values
 
 
 @pytest.mark.parametrize("name", ["exp2", "log"])
 def test_config_c5_full_scale_all_modes(cuda, oracle, name):
     """Config C5 at its stated size: 2^26 doubles on the paper's range
     (ref: PAPER.md:194) + 2^24 wide-range + 2^24 random bit
-    patterns, all four modes, device path, bit-exact vs the oracle."""
+    patterns (+ 2^23 log inputs within 2^-9 of 1), all four modes, device path,
+    bit-exact vs the oracle."""
     x = _c5_inputs(name, 26 if name == "exp2" else 27)
     want = oracle.f64(name, x.view(np.uint64), None)
     xt = cuda.from_numpy(x).cuda()

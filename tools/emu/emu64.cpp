@@ -52,3 +52,19 @@ extern "C" int emu64_acc(int fn, const double *x, double *y, uint64_t n, uint64_
   }
   return 0;
 }
+// fast-path value and round-test bound (tools/certify_f64.py dense-grid check):
+// exp2: V (2^x = V 2^N), b = EPS_EXP2D |V.hi|, n_out = N; log: V, b, n_out = 0
+extern "C" int emu64_value(int fn, const double *x, double *hi, double *lo, double *b, int *nout,
+                           uint64_t n) {
+  init();
+  for (uint64_t i = 0; i < n; ++i) {
+    if (fn == 0) {
+      Exp2dV e = exp2d_value(x[i], T);
+      hi[i] = e.V.hi; lo[i] = e.V.lo; b[i] = EPS_EXP2D * dabs(e.V.hi); nout[i] = e.N;
+    } else {
+      LogdV v = logd_value(x[i], 0, T);
+      hi[i] = v.V.hi; lo[i] = v.V.lo; b[i] = v.b; nout[i] = 0;
+    }
+  }
+  return 0;
+}

@@ -7,7 +7,9 @@
    within 2^-THR (relative) of a binary64 rounding boundary;
 2. every candidate is re-measured with the reference's own
    boundary_distance_f64 (ref: proj/src/oracle.cpp:502-563, compiled
-   unmodified into oracle/_ref/libcrvec_ref.so) and the TOP closest are kept;
+   unmodified into oracle/_ref/libcrvec_ref.so; an ABSOLUTE distance x 2^160),
+   normalised by ulp(f(x)) so exp2's tiny results do not dominate, and the TOP
+   closest are kept;
 3. expected outputs in all four modes come from the reference's
    ziv_correctly_round_f64 (ref: proj/src/oracle.cpp:326-345) and are checked
    equal to the oracle restatement's.
@@ -31,8 +33,11 @@ sys.path.insert(0, ROOT)
 import paper_2605_15547_b200 as crvec  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
-RANGES = {"exp2": [(-20.0, 20.0, 0.75), (-1022.0, 1024.0, 0.25)],
-          "log": [(0.125, 8.0, 0.75), ("bits", None, 0.25)]}
+# (lo, hi, fraction of the screen); "bits": random positive normal patterns.
+# Near 1 (log) / near 0 (exp2) the value is r-dominated: the regime where the
+# fast path's r^3-term rounding errors matter most.
+RANGES = {"exp2": [(-20.0, 20.0, 0.625), (-1022.0, 1024.0, 0.25), (-2.0 ** -10, 2.0 ** -10, 0.125)],
+          "log": [(0.125, 8.0, 0.5), ("bits", None, 0.125), (1 - 2.0 ** -8, 1 + 2.0 ** -8, 0.375)]}
 
 
 def screen_inputs(name, n, gen):
@@ -100,24 +105,33 @@ def main():
         t_scan = time.time() - t0
         cx = np.unique(cx)
         bd = ref_boundary_distance(name, cx)
-        rows = sorted((d, float(x)) for x, (d, ex, dom) in zip(cx, bd) if dom and not ex)
-        top = rows[: a.top]
-        xs = np.array([x for _, x in top], dtype=np.float64)
+        keep = np.array([dom and not ex for d, ex, dom in bd], dtype=bool)
+        cx = cx[keep]
+        dabs = np.array([d for d, ex, dom in bd], dtype=np.float64)[keep]
+        yrn = O.ref_f64(name, cx.view(np.uint64), 0).view(np.float64)
+        ulp = np.spacing(np.abs(yrn))
+        dulp = dabs * 2.0 ** -160 / ulp  # reference distance in ulps of the result
+        order = np.argsort(dulp, kind="stable")[: a.top]
+        top = [(float(dulp[i]), float(cx[i]), float(dabs[i])) for i in order]
+        xs = np.array([x for _, x, _ in top], dtype=np.float64)
         want = np.stack([O.ref_f64(name, xs.view(np.uint64), m) for m in range(4)], axis=1)
         mine = O.f64(name, xs.view(np.uint64), None)
         assert (mine == want).all(), "oracle restatement disagrees with the reference on the hard set"
         np.savez_compressed(os.path.join(a.out, f"{name}.npz"), x=xs.view(np.uint64),
-                            dist=np.array([d for d, _ in top]), want=want)
+                            dist=np.array([d for _, _, d in top]), dist_ulp=np.array([u for u, _, _ in top]),
+                            want=want)
         meta = {"fn": name, "screen_inputs": 1 << a.screen, "ranges": [list(map(str, r)) for r in RANGES[name]],
                 "seed": 5 + fid, "rng": f"torch {torch.__version__} cuda Generator",
                 "fast_path_threshold": f"2^-{a.thr:g} relative", "candidates": total,
-                "kept": len(top), "rank": "reference boundary_distance_f64 (x 2^160), ref: proj/src/oracle.cpp:502-563",
+                "kept": len(top), "rank": "reference boundary_distance_f64 (x 2^160, ref: proj/src/oracle.cpp:502-563) "
+                                          "/ ulp(f(x)), ascending",
                 "expected": "reference ziv_correctly_round_f64, 4 modes (== oracle restatement)",
-                "hardest_dist_x2^160": top[0][0] if top else None, "screen_seconds": round(t_scan, 2)}
+                "hardest_dist_ulps": top[0][0] if top else None,
+                "kept_dist_ulps_max": top[-1][0] if top else None, "screen_seconds": round(t_scan, 2)}
         with open(os.path.join(a.out, f"{name}.json"), "w") as f:
             json.dump(meta, f, indent=1)
         print(f"{name}: screen {t_scan:.1f}s, {total} candidates, kept {len(top)}, "
-              f"hardest d*2^160 = {meta['hardest_dist_x2^160']}", flush=True)
+              f"hardest {meta['hardest_dist_ulps']:.3g} ulp, 512th {meta['kept_dist_ulps_max']:.3g} ulp", flush=True)
 
 
 if __name__ == "__main__":
