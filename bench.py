@@ -17,14 +17,17 @@ Inputs are 1 GiB per function (> 126 MB L2), so no L2 flush is needed.
   roofline   the dominant kernel (logf's k_map_vec): 8 algorithmic bytes per
              element x 2^28 / its average event-timed duration vs the measured
              HBM copy bandwidth of MEASURED_PEAKS.json.
-  cpu_baseline  the reference's own CPU path (ziv_correctly_round_f32 of the
-             reference oracle compiled by `make -C oracle ref`, FuncId::log) on
-             a bounded sample of the same inputs, all host threads, rank 0.
+  cpu_baseline  the reference's own CPU kernel on the path, cr_log2f<16>
+             (Backend::vector; compiled unmodified from the reference's sources
+             with generated tables by `make -C oracle ref`), on a bounded sample
+             of the config-2 log2f input, all host threads, rank 0; its 1-core
+             rate and the reference oracle's rate beside it.
   sweep      exhaustive 2^32 x 4-mode sweep of all 19 functions, sharded by
              chunk range across ranks, one NCCL all_reduce of the per-chunk
              hashes; seconds (max over ranks) and mismatching chunks vs golden.
 
---impl reference times the reference CPU path alone (rank 0; other ranks exit).
+--impl reference times the reference's cr_log2f<16> alone on the host cores
+(rank 0; other ranks exit 0).
 """
 from __future__ import annotations
 
@@ -48,10 +51,15 @@ N_ELEM = 1 << 28
 
 def ncu_traffic(fn: str):
     """DRAM bytes (read + write) per launch of k_map_vec<fn> from the committed
-    `ncu --set full` capture (profiles/r01/ncu_full_<fn>.csv), or None."""
+    `ncu --set full` capture (profiles/rNN/ncu_full_<fn>.csv, latest round), or None."""
     import csv
-    p = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{fn}.csv")
-    if not os.path.exists(p):
+    p = None
+    for rnd in ("r02", "r01"):
+        c = os.path.join(ROOT, "profiles", rnd, f"ncu_full_{fn}.csv")
+        if os.path.exists(c):
+            p = c
+            break
+    if p is None:
         return None
     try:
         rows = list(csv.reader(open(p)))
@@ -120,11 +128,32 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        # the sampler is live (NVML initialised, one sample taken) before the
+        # timed region starts, so even a short region is sampled
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 10 and self._t.is_alive():
+            time.sleep(0.001)
+        self._n0 = len(self.samples)
         return self
 
+    def sample_now(self):
+        """One synchronous sample (taken at the end of the timed region)."""
+        try:
+            import pynvml
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                 pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                 pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        except Exception:
+            pass
+
     def __exit__(self, *a):
+        self.sample_now()
         self._stop.set()
         self._t.join(timeout=10)
+        # keep the samples taken during the region (plus the one at its end)
+        if len(self.samples) > self._n0:
+            self.samples = self.samples[self._n0:]
 
     def summary(self):
         if not self.samples:
@@ -135,18 +164,45 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": "nvml 5 ms"}
 
 
-def dist_init():
+def dist_init(backend: str = "nccl"):
+    """One process per GPU (torchrun env). NCCL over NVLink on GPUs; gloo for
+    the CPU self-test of the launch / shard / reduce path."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # create the communicator now (untimed): one tiny collective
+            t = torch.ones(1, device="cuda")
+            dist.all_reduce(t)
+            torch.cuda.synchronize()
+        else:
+            dist.init_process_group("gloo")
+        dist.barrier()
+    elif backend == "nccl" and torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
+
+
+def self_launch(argv, n: int) -> int:
+    """`bench.py --gpus N` run as a plain process (no torchrun environment):
+    re-exec under torch.distributed.run with N ranks on this node, rendezvous on
+    127.0.0.1, and return the launcher's exit status."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")         # communicator lines (nranks) for the record
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    return subprocess.run(cmd, env=env).returncode
 
 
 def barrier(world):
@@ -166,42 +222,96 @@ def max_over_ranks(v: float, world: int) -> float:
 
 
 # ------------------------------------------------------------ reference arm --
-def cpu_reference(fn_oracle: str, sample: int, threads: int = 0):
-    """Time the reference's own CPU path (ziv_correctly_round_f32, RNE)."""
+REF_WORKLOAD = ("log2f over the config-2 log-family input distribution (tests/inputs.py log_family_input, "
+                "seed 4), RNE, through the reference's cr_log2f<16> (Backend::vector) -- log2f is the "
+                "only log-family function the reference implements (ref: proj/src/kernels_f32.cpp:119-191); "
+                "std::thread over 16K-element chunks, all host cores")
+
+
+def cpu_reference_kernel(sample: int, threads: int = 0, vector: bool = True):
+    """The reference's own CPU kernel on the path: cr_log2f<16> (Backend::vector,
+    compiled unmodified from /root/reference with generated tables into
+    oracle/_ref/libcrvec_refk*.so), over a sample of the config-2 log2f input.
+    Returns (Gelem/s, seconds)."""
+    from oracle import oracle as O
+    from tests.inputs import log_family_input
+    x = log_family_input("log2f", sample, seed=4)
+    O.refk_f32("log2", x[:4096], 0, threads, vector)  # warm the thread pool / tables
+    t0 = time.perf_counter()
+    O.refk_f32("log2", x, 0, threads, vector)
+    dt = time.perf_counter() - t0
+    return sample / dt / 1e9, dt
+
+
+def cpu_reference_oracle(sample: int, threads: int = 0):
+    """The reference's Ziv oracle (ziv_correctly_round_f32, FuncId::log), the
+    only reference CPU path for logf. Returns (Gelem/s, seconds)."""
     from oracle import oracle as O
     from tests.inputs import log_family_input
     x = log_family_input("logf", sample, seed=3)
-    use_ref = O.ref_available() and fn_oracle in O.REF_FNS
     t0 = time.perf_counter()
-    if use_ref:
-        O.ref_f32(fn_oracle, x, 0, threads)
-    else:
-        O.f32(fn_oracle, x, 0, threads, use_ld=False)
+    O.ref_f32("log", x, 0, threads)
     dt = time.perf_counter() - t0
-    return sample / dt / 1e9, ("reference" if use_ref else "port"), dt
+    return sample / dt / 1e9, dt
+
+
+def cpu_baseline_record(sample: int):
+    """cpu_baseline: the reference's vector kernel on all host cores (value),
+    with its 1-thread rate and the reference oracle's rate beside it."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    if not O.refk_available():
+        v, dt = cpu_reference_oracle(min(sample, 1 << 21))
+        return {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "reference",
+                "sample": f"reference oracle ziv_correctly_round_f32(log), {min(sample, 1 << 21)} elements, {dt:.2f} s"}
+    v, dt = cpu_reference_kernel(sample)
+    v1, dt1 = cpu_reference_kernel(sample // 16, threads=1)
+    vo, dto = cpu_reference_oracle(1 << 20)
+    return {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "reference",
+            "sample": f"{sample} elements of the config-2 log2f input through cr_log2f<16> "
+                      f"(Backend::vector), {dt:.2f} s on {cores} threads",
+            "paths": {"cr_log2f<16> vector, all cores": {"gelem_s": v, "cores": cores},
+                      "cr_log2f<16> vector, 1 core": {"gelem_s": v1, "cores": 1},
+                      "ziv_correctly_round_f32(log) oracle, all cores": {"gelem_s": vo, "cores": cores}},
+            "isa": os.path.basename(O.refk_path() or "")}
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the reference's own CPU implementation of the path on the
+    box's host cores (rank 0 only; other ranks exit 0 without work). One step =
+    one bounded sample of the workload through cr_log2f<16>."""
     if rank != 0:
         return
+    from oracle import oracle as O
     cores = os.cpu_count() or 1
-    sample = args.cpu_sample
-    vals = []
+    sample = args.ref_sample
+    if not O.refk_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcrvec_refk*.so not built "
+                          "(make -C oracle ref with /root/reference present)"}), flush=True)
+        return
     for _ in range(args.warmup):
-        cpu_reference("log", sample)
+        cpu_reference_kernel(sample)
+    ts = []
     for _ in range(args.steps):
-        v, kind, _ = cpu_reference("log", sample)
-        vals.append(v)
-    value = float(np.median(vals))
+        _, dt = cpu_reference_kernel(sample)
+        ts.append(dt)
+    secs = float(np.sum(ts))
+    value = sample * args.steps / secs / 1e9
+    v1, _ = cpu_reference_kernel(max(1 << 16, sample // 16), threads=1)
+    vo, dto = cpu_reference_oracle(1 << 20)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gelem/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sample / (value * 1e9) * 1e3, "higher_is_better": True,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "logf (FuncId::log) over the config-2 log-family input distribution, RNE",
-                   "sample_elems_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "Gelem/s", "cores": cores, "kind": kind,
-                         "sample": f"{sample} elements of the 2^28 config-2 logf input per step"},
+        "config": {"workload": REF_WORKLOAD, "sample_elems_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "Gelem/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample} elements of the config-2 log2f input per step",
+                         "paths": {"cr_log2f<16> vector, all cores": {"gelem_s": value, "cores": cores},
+                                   "cr_log2f<16> vector, 1 core": {"gelem_s": v1, "cores": 1},
+                                   "ziv_correctly_round_f32(log) oracle, all cores": {"gelem_s": vo,
+                                                                                       "cores": cores}},
+                         "isa": os.path.basename(O.refk_path() or "")},
         "e2e": {"value": value, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,8 +320,12 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------ sweep ----
 def run_sweep(rank, world, fns):
     """Exhaustive 2^32 x 4-mode sweep of `fns`: chunk ranges sharded across
-    ranks (paper_2605_15547_b200/sweep.py), one all_reduce (NCCL) of the
-    per-chunk hash table; seconds = max over ranks of the device time."""
+    ranks (paper_2605_15547_b200/sweep.py run_device): the sweep kernels
+    accumulate every function's chunk hashes into ONE device table, then ONE
+    NCCL all_reduce; no host round trip or per-function synchronisation inside
+    the timed region. Seconds = max over ranks of the device time from the
+    first sweep launch to the end of the all_reduce (communicator created
+    before, untimed); one D2H copy of the table after the region."""
     import torch
     import paper_2605_15547_b200 as crvec
     from paper_2605_15547_b200 import sweep
@@ -220,14 +334,59 @@ def run_sweep(rank, world, fns):
     s = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(s)
-    rows, table, _ = sweep.run(fns, sweep.gpu_evaluator(), rank, world, device="cuda")
+    rows, table, _ = sweep.run_device(fns, rank, world)
     ev1.record(s)
     torch.cuda.synchronize()
     secs = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
-    res = sweep.compare(rows, table, ROOT, crvec.ORACLE_NAME)
+    host = table.cpu().numpy().view(np.uint64)
+    res = sweep.compare(rows, host, ROOT, crvec.ORACLE_NAME) if rank == 0 else {}
     mism = sum(len(v) for v in res.values() if v is not None)
     checked = sum(1 for v in res.values() if v is not None)
-    return secs, mism, checked
+    return secs, mism, checked, len(rows)
+
+
+def run_selftest(args, rank, world):
+    """CPU self-test of the multi-rank plumbing bench.py uses on GPUs (gloo):
+    self-launch, chunk sharding, one all_reduce of the hash table, max-over-
+    ranks timing. Each rank fills its shard with a deterministic stand-in hash
+    (no kernels, no oracle), rank 0 checks the reduced table equals the full
+    single-rank table. Prints one JSON line."""
+    import torch
+    from paper_2605_15547_b200 import sweep
+
+    def fill(names, lo, hi):
+        c = np.arange(lo, hi, dtype=np.uint64)[:, None] * np.uint64(4) + np.arange(4, dtype=np.uint64)[None]
+        return [torch.from_numpy((c * np.uint64(0x9E3779B97F4A7C15 + k)).view(np.int64)) for k in range(len(names))]
+
+    names = ["logf", "log2f", "sincosf"]
+    rows = sweep.rows_for(names)
+    t0 = time.perf_counter()
+    table = torch.zeros((len(rows), sweep.CHUNKS, 4), dtype=torch.int64)
+    lo, hi = sweep.shard(rank, world)
+    for i, part in enumerate(fill(rows, lo, hi)):
+        table[i, lo:hi] = part
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(table)
+    secs = max_over_ranks_cpu(time.perf_counter() - t0, world)
+    if rank == 0:
+        full = torch.stack([p for p in fill(rows, 0, sweep.CHUNKS)])
+        mism = int((table != full).any(dim=2).sum())
+        print(json.dumps({"metric": METRIC, "value": None, "selftest": True, "n_gpus": world,
+                          "backend": "gloo", "sweep": {"seconds": secs, "ranks": world, "rows": len(rows),
+                                                       "mismatching_chunks": mism,
+                                                       "collective": "one all_reduce of the hash table"}}),
+              flush=True)
+
+
+def max_over_ranks_cpu(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def _libm_ops():
@@ -242,7 +401,7 @@ def _libm_ops():
 LIBM_OPS = {}
 
 
-def all_functions_table(n=1 << 28, reps=5):
+def all_functions_table(n=1 << 28, reps=9):
     """Device throughput of every binary32 function (and the binary64 pair) at
     2^28 (2^26 for binary64), inputs generated on the device: the configs'
     distributions for the log and trig families, uniform over each function's
@@ -306,6 +465,7 @@ def run_crvec(args, rank, world, local):
     import ctypes
     import torch
     import paper_2605_15547_b200 as crvec
+    from paper_2605_15547_b200.sweep import shard
     from tests.inputs import log_family_input
 
     L = crvec.lib()
@@ -378,18 +538,19 @@ def run_crvec(args, rank, world, local):
     # ---- exhaustive sweep (sharded across ranks)
     sweep = None
     if not args.no_sweep:
-        secs_sw, mism, checked = run_sweep(rank, world, crvec.F32_FUNCS + ["sincosf"])
+        secs_sw, mism, checked, nrows = run_sweep(rank, world, crvec.F32_FUNCS + ["sincosf"])
         sweep = {"seconds": secs_sw, "functions": 19, "modes": 4, "patterns": 2 ** 32,
                  "mismatching_chunks": mism, "golden_sets_checked": checked, "ranks": world,
-                 "collective": "one NCCL all_reduce of 20x4096x4 u64 chunk hashes" if world > 1 else None}
+                 "chunks_per_rank": [b - a for a, b in (shard(r, world) for r in range(world))],
+                 "collective": (f"one NCCL all_reduce of the {nrows}x4096x4 u64 chunk-hash table"
+                                if world > 1 else None),
+                 "timed": "first sweep launch .. end of the all_reduce, device events, max over ranks"}
 
     table = all_functions_table() if (rank == 0 and not args.no_table) else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, kind, dt = cpu_reference("log", args.cpu_sample)
-        cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": kind,
-               "sample": f"{args.cpu_sample} elements of the config-2 logf input (RNE), {dt:.1f} s"}
+        cpu = cpu_baseline_record(args.ref_sample)
 
     launches = len(fns) * args.steps
     if rank == 0:
@@ -424,17 +585,27 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="crvec", choices=["crvec", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=1 << 21)
+    ap.add_argument("--ref-sample", type=int, default=1 << 24,
+                    help="elements per reference-arm step (cr_log2f<16> on the host cores)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-table", action="store_true")
+    ap.add_argument("--selftest", action="store_true",
+                    help="CPU (gloo) self-test of the multi-rank launch / shard / reduce path")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))
         return
-    rank, world, local = dist_init()
-    run_crvec(args, rank, world, local)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
+    rank, world, local = dist_init("gloo" if args.selftest else "nccl")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.selftest:
+        run_selftest(args, rank, world)
+    else:
+        run_crvec(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -40,10 +40,59 @@ _ref = None
 _refk = None
 
 
+REF_ARTIFACT = os.path.join(os.path.dirname(HERE), "tests", "golden", "ref_tables.txt")
+REF_GEN_INC = os.path.join(HERE, "_ref", "gen", "tables_data.inc")
+
+
+def inc_from_artifact(path: str = REF_ARTIFACT, out: str = REF_GEN_INC) -> None:
+    """The statements the reference's builtin_tables() includes
+    (ref: proj/src/tables.cpp:233-240), from its text artifact
+    (ref: proj/src/tables.cpp:75-120; tests/golden/ref_tables.txt, written by
+    tools/gen_ref_tables.py through the reference's own serialize_tables)."""
+    def f(h):
+        return float(np.array([int(h, 16)], dtype=np.uint64).view(np.float64)[0]).hex()
+    lines = ["// from " + os.path.relpath(path, os.path.dirname(HERE)) + " (oracle.inc_from_artifact)"]
+    meta = {"fit.exp2f": "fit_exp2f", "fit.log2f": "fit_log2f", "fit.exp2d": "fit_exp2d", "fit.logd": "fit_logd",
+            "eps.exp2d": "eps_exp2d", "eps.logd": "eps_logd", "quant.logd": "quant_logd"}
+    for ln in open(path):
+        if not ln.strip() or ln.startswith("#"):
+            continue
+        key, *v = ln.split()
+        k = key.split(".")
+        if key.startswith(("exp2f.T.", "exp2f.c.", "logd.rcp.")):
+            lines.append(f"v.{k[0]}.{k[1]}[{k[2]}] = {f(v[0])};")
+        elif key.startswith("log2f.c."):
+            lines.append(f"v.log2f.c[{k[2]}][{k[3]}] = {f(v[0])};")
+        elif k[0] == "exp2d" and k[1] in ("T1", "T2", "T3"):
+            lines.append(f"v.exp2d.{k[1]}_hi[{k[2]}] = {f(v[0])}; v.exp2d.{k[1]}_lo[{k[2]}] = {f(v[1])};")
+        elif key in ("exp2d.ln2", "logd.ln2"):
+            lines.append(f"v.{k[0]}.ln2 = DD{{{f(v[0])}, {f(v[1])}}};")
+        elif key.startswith("exp2d.c."):
+            lines.append(f"v.exp2d.c[{int(k[2]) - 2}] = {f(v[0])};")
+        elif key.startswith("logd.c."):
+            lines.append(f"v.logd.c[{int(k[2]) - 3}] = {f(v[0])};")
+        elif key.startswith("logd.L."):
+            u = int(v[0], 16)
+            lines.append(f"v.logd.L[{k[2]}] = static_cast<std::int64_t>({u - (1 << 64) if u >> 63 else u}LL);")
+        elif key == "logd.degree":
+            lines.append(f"v.logd.tail_degree = {int(v[0])};")
+        elif key.startswith("meta."):
+            lines.append(f"v.eps.{meta[key[5:]]} = {f(v[0])};")
+        else:
+            raise ValueError("unknown table record " + key)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
 def build(ref: bool = True) -> None:
-    """Compile the oracle (and the reference oracle when /root/reference exists)."""
+    """Compile the oracle (and, when /root/reference exists, the reference's
+    oracle and kernels; the kernels' table data comes from the committed
+    artifact tests/golden/ref_tables.txt)."""
     subprocess.run(["make", "-s", "-C", HERE, "libcrvec_oracle.so"], check=True)
     if ref and os.path.isdir("/root/reference/proj"):
+        if not os.path.exists(REF_GEN_INC) and os.path.exists(REF_ARTIFACT):
+            inc_from_artifact()
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
 
 

@@ -41,7 +41,7 @@ def run(names: Sequence[str], evaluator: Evaluator, rank: int = 0, world: int = 
     Returns (table: uint64 [len(names) (+1 if sincosf), chunks, 4], seconds
     measured around compute + collective on this rank)."""
     import torch
-    rows = list(names) + (["sincosf:cos"] if "sincosf" in names else [])
+    rows = rows_for(names)
     table = torch.zeros((len(rows), chunks, 4), dtype=torch.int64, device=device)
     lo, hi = shard(rank, world, chunks)
     t0 = time.perf_counter()
@@ -62,6 +62,46 @@ def run(names: Sequence[str], evaluator: Evaluator, rank: int = 0, world: int = 
         torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     return rows, table.cpu().numpy().view(np.uint64), secs
+
+
+def rows_for(names: Sequence[str]) -> List[str]:
+    """Table rows: one per function, plus the cos half of sincosf."""
+    return list(names) + (["sincosf:cos"] if "sincosf" in names else [])
+
+
+def run_device(names: Sequence[str], rank: int = 0, world: int = 1, chunks: int = CHUNKS,
+               force_accurate: bool = False, reduce: bool = True, stream=None):
+    """Device-resident sweep (the GPU path bench.py times): every function's
+    chunk hashes are accumulated by the crvec_sweep_f32 kernels straight into
+    one zeroed [rows, chunks, 4] int64 tensor on this rank's GPU (no host round
+    trip, no per-function synchronisation), then ONE all_reduce(sum) over NCCL.
+
+    Returns (rows, table tensor on the device, accurate-lane counter tensor).
+    The caller copies the table to the host once, after its timing events."""
+    import ctypes
+
+    import torch
+    import paper_2605_15547_b200 as crvec
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rows = rows_for(names)
+    table = torch.zeros((len(rows), chunks, 4), dtype=torch.int64, device=dev)
+    ctr = torch.zeros(4, dtype=torch.int64, device=dev)
+    lo, hi = shard(rank, world, chunks)
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    sp = ctypes.c_void_p(s.cuda_stream)
+    L = crvec.lib()
+    if hi > lo:
+        for i, name in enumerate(names):
+            h2 = table[rows.index("sincosf:cos"), lo].data_ptr() if name == "sincosf" else None
+            rc = L.crvec_sweep_f32(crvec.FN_IDS[name], lo, hi, table[i, lo].data_ptr(), h2, ctr.data_ptr(),
+                                   int(force_accurate), sp)
+            if rc != 0:
+                raise crvec.CrvecError(f"crvec_sweep_f32({name}) failed: {rc}")
+    if reduce and world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(table)  # sum mod 2^64: chunk hashes are disjoint per rank
+    return rows, table, ctr
 
 
 def golden_path(root: str, name: str) -> str:

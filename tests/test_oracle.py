@@ -247,3 +247,59 @@ def test_hardcase_corpus_expected_outputs(oracle):
         x = np.array([int(r[0], 16) for r in rows], np.uint32)
         want = np.array([[int(v, 16) for v in r[3:7]] for r in rows], np.uint32)
         assert (oracle.f32(crvec.ORACLE_NAME[name], x, None, use_ld=False) == want).all(), name
+
+
+# ---- the reference's own kernels (oracle/_ref/libcrvec_refk*.so) ----------
+@pytest.fixture(scope="module")
+def refk(ref_oracle):
+    O = ref_oracle
+    if not O.refk_available():
+        pytest.skip("reference kernels not built")
+    return O
+
+
+def test_reference_table_artifact_roundtrip(refk):
+    """tests/golden/ref_tables.txt is the reference's own text artifact
+    (serialize_tables, FNV-1a header): its parse_tables accepts it and it equals
+    the tables compiled into the reference kernels (ref: proj/src/tables.cpp:75-226)."""
+    K = refk.refk()
+    assert K.crvec_refk_tables_from_file(refk.REF_ARTIFACT.encode()) == 0
+    assert K.crvec_refk_file_equals_builtin() == 1
+    assert K.crvec_refk_tables_loaded() == 1
+
+
+def test_reference_kernels_with_generated_tables_match_oracle(refk):
+    """SPEC acceptance spot check (ref: SPEC.md:637): the reference's cr_exp2f /
+    cr_log2f (both backends) and cr_exp2 / cr_log, run with the generated
+    tables, agree with the oracle in all four modes."""
+    O = refk
+    rng = np.random.default_rng(777)
+    x32 = np.concatenate([rng.integers(0, 2 ** 32, 3000, dtype=np.uint64).astype(np.uint32),
+                          rng.uniform(-150, 130, 3000).astype(np.float32).view(np.uint32)])
+    for fn in ("exp2", "log2"):
+        want = O.f32(fn, x32, None)
+        for m in range(4):
+            for vec in (True, False):
+                assert (O.refk_f32(fn, x32, m, vector=vec) == want[:, m]).all(), (fn, m, vec)
+    x64 = {"exp2": np.concatenate([rng.uniform(-20, 20, 2000), rng.uniform(-1075, 1024, 1000)]),
+           "log": np.concatenate([rng.uniform(0.125, 8, 2000),
+                                  rng.integers(1, 0x7FF0000000000000, 1000, dtype=np.uint64).view(np.float64)])}
+    for fn, xv in x64.items():
+        want = O.f64(fn, xv.view(np.uint64), None)
+        for m in range(4):
+            got, _ = O.refk_f64(fn, xv.view(np.uint64), m)
+            assert (got == want[:, m]).all(), (fn, m)
+
+
+def test_gpu_round_test_fixture_matches_live_reference(refk):
+    """tests/golden/ref_round_test.npz (the GPU round test's golden data) equals
+    the live reference round_test_lane on a sample."""
+    K = refk.refk()
+    g = np.load(os.path.join(ROOT, "tests", "golden", "ref_round_test.npz"))
+    v = ctypes.c_double()
+    for i in range(0, g["hi"].size, 37):
+        for m in range(4):
+            dec = K.crvec_refk_round_test_lane(float(g["hi"][i]), float(g["lo"][i]), int(g["scale"][i]),
+                                               float(g["eps_rel"][i]), float(g["eps_abs"][i]), m, ctypes.byref(v))
+            assert dec == g["decided"][i, m]
+            assert np.float64(v.value).view(np.uint64) == g["value"][i, m].view(np.uint64)
