@@ -77,8 +77,11 @@ int main() {
     v.hi.lane = {1.0, 2.0, 3.0, 1.0};
     v.lo.lane = {0.0, 0x1p-60, -0x1p-60, 0x1p-53};
     auto rt = round_test<4>(v, 0x1p-80, RoundingMode::TowardZero);
-    CHECK(!rt.decided[0] && rt.decided[1] && rt.decided[2] && !rt.decided[3]);
+    // lane 3: 1 + 2^-53 +- 2^-80 rounds to 1.0 toward zero at both ends (decided;
+    // the reference's round_test_lane agrees, oracle/_ref crvec_refk_round_test_lane)
+    CHECK(!rt.decided[0] && rt.decided[1] && rt.decided[2] && rt.decided[3]);
     CHECK(rt.fast_result[1] == 2.0 && rt.fast_result[2] == std::nextafter(3.0, 0.0));
+    CHECK(rt.fast_result[3] == 1.0);
     CHECK(rt.error_bound == 0x1p-80);
 
     // callout: the GPU accurate path

@@ -173,7 +173,7 @@ def test_extended_rung_never_changes_results(oracle):
 def test_golden_sweep_files_are_consistent(oracle):
     """Every committed sweep golden re-derives on a sampled chunk."""
     d = os.path.join(ROOT, "tests", "golden", "sweep")
-    names = sorted(f[:-4] for f in os.listdir(d) if f.endswith(".npy"))
+    names = sorted(f[:-4] for f in os.listdir(d) if f.endswith(".npy") and not f.startswith("."))
     assert names, "no golden sweep data"
     for fn in names:
         g = np.load(os.path.join(d, fn + ".npy"))
@@ -303,3 +303,21 @@ def test_gpu_round_test_fixture_matches_live_reference(refk):
                                                float(g["eps_rel"][i]), float(g["eps_abs"][i]), m, ctypes.byref(v))
             assert dec == g["decided"][i, m]
             assert np.float64(v.value).view(np.uint64) == g["value"][i, m].view(np.uint64)
+
+
+def test_golden_sweep_mpfr_only_dense_chunks(oracle):
+    """Re-derive seeded numerically dense chunks (|x| in [2^-10, 2^7): exponent
+    fields 117..134, chunk = pattern >> 20) of every committed exhaustive golden
+    with the MPFR-only Ziv ladder (the x87 long-double rung OFF), so the golden
+    hashes do not rest on glibc's *l() error bounds."""
+    d = os.path.join(ROOT, "tests", "golden", "sweep")
+    names = sorted(f[:-4] for f in os.listdir(d) if f.endswith(".npy") and not f.startswith("."))
+    rng = np.random.default_rng(20240817)
+    for fn in names:
+        g = np.load(os.path.join(d, fn + ".npy"))
+        for c in (int(rng.integers(117 * 8, 135 * 8)), 2048 + int(rng.integers(117 * 8, 135 * 8))):
+            p = np.arange(c << 20, (c + 1) << 20, dtype=np.uint64).astype(np.uint32)
+            y = oracle.f32(fn, p, None, use_ld=False)  # all host threads over elements
+            for m in range(4):
+                h = oracle.mix64((y[:, m].astype(np.uint64) << np.uint64(32)) | p.astype(np.uint64))
+                assert np.uint64(h.sum(dtype=np.uint64)) == g[c, m], (fn, c, m)

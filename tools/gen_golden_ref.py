@@ -7,8 +7,8 @@ into oracle/_ref/libcrvec_ref.so by `make -C oracle ref`). Test-data tool.
 The result replaces tests/golden/sweep/<fn>.npy only if it equals the
 restatement's hashes chunk for chunk (otherwise it stops and reports the
 differing chunks); the provenance JSON then records "source": "reference build".
-Progress is checkpointed to tests/golden/sweep/.<fn>.ref.partial.npy, so an
-interrupted run resumes.
+Progress is checkpointed to oracle/_ref/golden_partial/<fn>.ref.partial.npy
+(git-ignored, outside the fixture directory), so an interrupted run resumes.
 
 Usage: python tools/gen_golden_ref.py [exp2 log log2] [--threads T] [--step CHUNKS]
 """
@@ -25,6 +25,7 @@ sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "sweep")
+PARTIAL = os.path.join(ROOT, "oracle", "_ref", "golden_partial")
 
 
 def ref_lib():
@@ -54,7 +55,8 @@ def main():
     fns = args or ["exp2", "log", "log2"]
     L = ref_lib()
     for fn in fns:
-        part = os.path.join(OUT, f".{fn}.ref.partial.npy")
+        os.makedirs(PARTIAL, exist_ok=True)
+        part = os.path.join(PARTIAL, f"{fn}.ref.partial.npy")
         h = np.load(part) if os.path.exists(part) else np.zeros((4096, 4), dtype=np.uint64)
         done = np.load(part + ".done.npy") if os.path.exists(part + ".done.npy") else np.zeros(4096, bool)
         t0 = time.time()

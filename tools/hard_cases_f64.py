@@ -110,7 +110,7 @@ def main():
         dabs = np.array([d for d, ex, dom in bd], dtype=np.float64)[keep]
         yrn = O.ref_f64(name, cx.view(np.uint64), 0).view(np.float64)
         ulp = np.spacing(np.abs(yrn))
-        dulp = dabs * 2.0 ** -160 / ulp  # reference distance in ulps of the result
+        dulp = (dabs / ulp) * 2.0 ** -160  # reference distance in ulps of the result (divide first: no underflow)
         order = np.argsort(dulp, kind="stable")[: a.top]
         top = [(float(dulp[i]), float(cx[i]), float(dabs[i])) for i in order]
         xs = np.array([x for _, x, _ in top], dtype=np.float64)
