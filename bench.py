@@ -400,6 +400,19 @@ def _libm_ops():
 
 LIBM_OPS = {}
 
+# Fast-path lookup tables + polynomial coefficients read per element, bytes
+# (csrc/crvec_tables.inc; shared-memory pair tables counted at their 16-byte
+# entries). The paper reports its table footprint beside the timings
+# (ref: SPEC.md:629-634); the reference's own sizes are in REF_TABLE_BYTES.
+TABLE_BYTES = {
+    "expf": 160, "exp2f": 160, "exp10f": 160, "expm1f": 168, "sinhf": 160, "coshf": 160,
+    "tanhf": 168, "logf": 304, "log2f": 304, "log10f": 304, "log1pf": 304,
+    "sinf": 304, "cosf": 304, "tanf": 304, "sincosf": 304, "asinf": 544, "acosf": 544,
+    "atanf": 352, "rsqrtf": 0, "exp2(f64)": 2080, "log(f64)": 12344,
+}
+PH_TABLE_BYTES = 3712  # Payne-Hanek 16/pi chunk table (trig big-argument path only)
+REF_TABLE_BYTES = {"exp2f": 120, "log2f": 640, "exp2(f64)": 816, "log(f64)": 1104}  # ref: proj/src/tables.cpp:228-231
+
 
 def all_functions_table(n=1 << 28, reps=9):
     """Device throughput of every binary32 function (and the binary64 pair) at
@@ -449,6 +462,17 @@ def all_functions_table(n=1 << 28, reps=9):
         if op is not None:
             tl = timed(lambda: op(x, out=y))
             out[name]["torch_libm_gelem_s"] = round(n / tl / 1e9, 1)
+        elif name == "exp10f":  # no torch exp10: CUDA powf(10, x), the library's 1-ulp path
+            tl = timed(lambda: torch.pow(10.0, x, out=y))
+            out[name]["torch_libm_gelem_s"] = round(n / tl / 1e9, 1)
+            out[name]["torch_libm_op"] = "torch.pow(10, x)"
+        elif name == "sincosf":  # two library launches (sin, cos) for the two outputs
+            tl = timed(lambda: (torch.sin(x, out=y), torch.cos(x, out=y2)))
+            out[name]["torch_libm_gelem_s"] = round(n / tl / 1e9, 1)
+            out[name]["torch_libm_op"] = "torch.sin + torch.cos"
+        out[name]["table_bytes"] = TABLE_BYTES[name] + (PH_TABLE_BYTES if name in ("sinf", "cosf", "tanf", "sincosf") else 0)
+        if name in REF_TABLE_BYTES:
+            out[name]["ref_table_bytes"] = REF_TABLE_BYTES[name]
         del x
     n64 = 1 << 26
     for name, lo, hi in (("exp2", -20.0, 20.0), ("log", 0.125, 8.0)):
@@ -456,7 +480,18 @@ def all_functions_table(n=1 << 28, reps=9):
         yy = torch.empty_like(x)
         f = getattr(L, f"crvec_{name}_dev")
         t = timed(lambda: f(x.data_ptr(), yy.data_ptr(), n64, 0, sp))
-        out[name + "(f64)"] = {"gelem_s": round(n64 / t / 1e9, 1), "frac_hbm": round(16 * n64 / t / 1e9 / peak, 3)}
+        k = name + "(f64)"
+        out[k] = {"gelem_s": round(n64 / t / 1e9, 1), "frac_hbm": round(16 * n64 / t / 1e9 / peak, 3)}
+        # Table IV analogue (ref: PAPER.md:229-234): the library's 1-ulp float64 kernel on the same array
+        op = torch.exp2 if name == "exp2" else torch.log
+        tl = timed(lambda: op(x, out=yy))
+        out[k]["torch_libm_gelem_s"] = round(n64 / tl / 1e9, 1)
+        out[k]["cr_over_libm_time"] = round(t / tl, 2)
+        out[k]["table_bytes"] = TABLE_BYTES[k]
+        out[k]["ref_table_bytes"] = REF_TABLE_BYTES[k]
+    for v in out.values():  # the paper's "cost of CR" column: CR time / library time
+        if "torch_libm_gelem_s" in v:
+            v["cr_over_libm_time"] = round(v["torch_libm_gelem_s"] / v["gelem_s"], 2)
     return out
 
 

@@ -257,6 +257,32 @@ __device__ __forceinline__ void resolve_rare_store(const float (&xs)[NE], unsign
   if (cnt) atomicAdd(counters, (unsigned long long)cnt);
 }
 
+// Rare path (staged form): the warp's lanes with pending slots write their NE
+// inputs to a per-thread shared-memory row (NE/4 128-bit stores) and each
+// resolves its own pending slots in a divergent loop (no select gather, no
+// warp-wide pass per slot depth), overwriting the one output float.
+template <class F, int M, int NE, int VW>
+__device__ __forceinline__ void resolve_rare_staged(const float (&xs)[NE], unsigned mask, float *yf,
+                                                    uint64_t fbase, unsigned long long *counters) {
+  __shared__ float4 stage[kThreads * (NE / 4)];
+  if (mask) {
+    float4 *row = stage + threadIdx.x * (NE / 4);
+#pragma unroll
+    for (int k = 0; k < NE / 4; ++k) row[k] = make_float4(xs[4 * k], xs[4 * k + 1], xs[4 * k + 2], xs[4 * k + 3]);
+    const float *rf = reinterpret_cast<const float *>(row);
+    int cnt = 0;
+    do {
+      const uint32_t e = (uint32_t)__ffs(mask) - 1u;
+      yf[fbase + (32u * VW * (e / VW) + (e % VW))] = u2f(resolve_one<F, M>(rf[e], cnt));
+      mask &= mask - 1u;
+    } while (mask);
+    if (cnt) atomicAdd(counters, (unsigned long long)cnt);
+  }
+}
+template <class F> struct RareStaged { static constexpr bool value = false; };
+template <int B> struct RareStaged<FnLogB<B>> { static constexpr bool value = true; };
+template <> struct RareStaged<FnLog1p> { static constexpr bool value = true; };
+
 template <class F, int M, int NE>
 __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)[NE],
                                            const typename F::Regs &R, PHBlock *sh,
@@ -301,6 +327,7 @@ template <bool A> struct RareStore<FnAsinAcos<A>> { static constexpr bool value 
 template <> struct RareStore<FnExpm1> { static constexpr bool value = true; };
 template <> struct RareStore<FnRsqrt> { static constexpr bool value = true; };
 template <> struct RareStore<FnTanh> { static constexpr bool value = true; };
+template <> struct RareStore<FnLog1p> { static constexpr bool value = true; };
 template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = true; };
 
 template <class F>
@@ -312,7 +339,7 @@ template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, m
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 2, minb = 3; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 1, minb = 3; };
-template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 1, minb = 4; };
+template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog2> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnSinh> { static constexpr int vw = 8, nv = 2, minb = 2; };
@@ -349,8 +376,12 @@ __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> 
       if (i < nv) st_vec<VW>(y + i, ys + VW * k);
       else mask &= ~(((1u << VW) - 1u) << (VW * k));  // stale inputs past the end
     }
-    if (__any_sync(kFull, mask != 0))
-      resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, (uint64_t)VW * base, counters);
+    if (__any_sync(kFull, mask != 0)) {
+      if constexpr (RareStaged<F>::value)
+        resolve_rare_staged<F, M, VW * NV, VW>(xs, mask, (float *)y, (uint64_t)VW * base, counters);
+      else
+        resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, (uint64_t)VW * base, counters);
+    }
   } else {
     eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
 #pragma unroll
