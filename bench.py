@@ -14,7 +14,7 @@ Inputs are 1 GiB per function (> 126 MB L2), so no L2 flush is needed.
   e2e        same metric through the C ABI host-pointer entry points
              (crvec_logf ... with pinned host buffers): every step includes the
              H2D copy of the inputs and the D2H copy of the results.
-  roofline   the dominant kernel (logf's k_map_vec): 8 algorithmic bytes per
+  roofline   the dominant kernel (the slowest of the four k_map_vec launches): 8 algorithmic bytes per
              element x 2^28 / its average event-timed duration vs the measured
              HBM copy bandwidth of MEASURED_PEAKS.json.
   cpu_baseline  the reference's own CPU kernel on the path, cr_log2f<16>
@@ -329,6 +329,9 @@ def run_sweep(rank, world, fns):
     import torch
     import paper_2605_15547_b200 as crvec
     from paper_2605_15547_b200 import sweep
+    # untimed warm-up: one chunk per function (shard 0 of 4096, no collective) so the
+    # sweep kernels are loaded (CUDA lazy module loading) before the timed region
+    sweep.run_device(fns, 0, sweep.CHUNKS, reduce=False)
     barrier(world)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
@@ -600,7 +603,7 @@ def run_crvec(args, rank, world, local):
                        "per_function_gelem_s": per_fn_gelem, "per_function_ms": fn_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(dom),
-                         "traffic_note": "dram read+write bytes per launch from profiles/r01/ncu_full_<fn>.csv "
+                         "traffic_note": "dram read+write bytes per launch from the latest profiles/rNN/ncu_full_<fn>.csv "
                                          f"(algorithmic {8 * n} B)",
                          "kernel": f"k_map_vec<{dom}> (8 B/elem x 2^28)", "peak_source": peak_kind},
             "cpu_baseline": cpu,

@@ -282,6 +282,8 @@ __device__ __forceinline__ void resolve_rare_staged(const float (&xs)[NE], unsig
 template <class F> struct RareStaged { static constexpr bool value = false; };
 template <int B> struct RareStaged<FnLogB<B>> { static constexpr bool value = true; };
 template <> struct RareStaged<FnLog1p> { static constexpr bool value = true; };
+template <> struct RareStaged<FnTanh> { static constexpr bool value = true; };
+template <> struct RareStaged<FnSinh> { static constexpr bool value = true; };
 
 template <class F, int M, int NE>
 __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)[NE],
@@ -328,6 +330,7 @@ template <> struct RareStore<FnExpm1> { static constexpr bool value = true; };
 template <> struct RareStore<FnRsqrt> { static constexpr bool value = true; };
 template <> struct RareStore<FnTanh> { static constexpr bool value = true; };
 template <> struct RareStore<FnLog1p> { static constexpr bool value = true; };
+template <> struct RareStore<FnSinh> { static constexpr bool value = true; };
 template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = true; };
 
 template <class F>
@@ -337,7 +340,7 @@ struct KernelShape {
 template <> struct KernelShape<FnExp2> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
-template <> struct KernelShape<FnExpm1> { static constexpr int vw = 4, nv = 2, minb = 3; };
+template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 2, minb = 2; };
