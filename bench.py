@@ -228,19 +228,25 @@ REF_WORKLOAD = ("log2f over the config-2 log-family input distribution (tests/in
                 "std::thread over 16K-element chunks, all host cores")
 
 
-def cpu_reference_kernel(sample: int, threads: int = 0, vector: bool = True):
+_REF_INPUT = {}
+
+
+def cpu_reference_kernel(sample: int, threads: int = 0, vector: bool = True, reps: int = 1):
     """The reference's own CPU kernel on the path: cr_log2f<16> (Backend::vector,
     compiled unmodified from /root/reference with generated tables into
-    oracle/_ref/libcrvec_refk*.so), over a sample of the config-2 log2f input.
-    Returns (Gelem/s, seconds)."""
+    oracle/_ref/libcrvec_refk*.so), `reps` passes over a sample of the config-2
+    log2f input (generated once per size). Returns (Gelem/s, seconds)."""
     from oracle import oracle as O
     from tests.inputs import log_family_input
-    x = log_family_input("log2f", sample, seed=4)
+    if sample not in _REF_INPUT:
+        _REF_INPUT[sample] = log_family_input("log2f", sample, seed=4)
+    x = _REF_INPUT[sample]
     O.refk_f32("log2", x[:4096], 0, threads, vector)  # warm the thread pool / tables
     t0 = time.perf_counter()
-    O.refk_f32("log2", x, 0, threads, vector)
+    for _ in range(reps):
+        O.refk_f32("log2", x, 0, threads, vector)
     dt = time.perf_counter() - t0
-    return sample / dt / 1e9, dt
+    return sample * reps / dt / 1e9, dt
 
 
 def cpu_reference_oracle(sample: int, threads: int = 0):
@@ -264,12 +270,12 @@ def cpu_baseline_record(sample: int):
         v, dt = cpu_reference_oracle(min(sample, 1 << 21))
         return {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "reference",
                 "sample": f"reference oracle ziv_correctly_round_f32(log), {min(sample, 1 << 21)} elements, {dt:.2f} s"}
-    v, dt = cpu_reference_kernel(sample)
+    v, dt = cpu_reference_kernel(sample, reps=4)  # ~10 core-seconds of the reference kernel
     v1, dt1 = cpu_reference_kernel(sample // 16, threads=1)
     vo, dto = cpu_reference_oracle(1 << 20)
     return {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "reference",
-            "sample": f"{sample} elements of the config-2 log2f input through cr_log2f<16> "
-                      f"(Backend::vector), {dt:.2f} s on {cores} threads",
+            "sample": f"4 passes over {sample} elements of the config-2 log2f input through cr_log2f<16> "
+                      f"(Backend::vector), {dt:.2f} s on {cores} threads ({dt * cores:.1f} core-s)",
             "paths": {"cr_log2f<16> vector, all cores": {"gelem_s": v, "cores": cores},
                       "cr_log2f<16> vector, 1 core": {"gelem_s": v1, "cores": 1},
                       "ziv_correctly_round_f32(log) oracle, all cores": {"gelem_s": vo, "cores": cores}},
@@ -623,7 +629,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="crvec", choices=["crvec", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=1 << 24,
+    ap.add_argument("--ref-sample", type=int, default=1 << 26,
                     help="elements per reference-arm step (cr_log2f<16> on the host cores)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -29,7 +29,27 @@ def main():
     for v in sys.argv[2:]:
         L = load(os.path.join(ROOT, "paper_2605_15547_b200", "variants", f"libcrvec_{v}.so"))
         bad = 0
-        for fn in fns:
+        for name in [f for f in fns if f in ("exp2d", "logd")]:  # binary64 pair
+            g = torch.Generator(device="cuda")
+            g.manual_seed(13)
+            lo, hi = (-20.0, 20.0) if name == "exp2d" else (0.125, 8.0)
+            xs = [torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * (hi - lo) + lo,
+                  torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device="cuda", dtype=torch.int64).view(torch.float64)]
+            for x in xs:
+                for m in range(4):
+                    outs = []
+                    for lib in (base, L):
+                        y = torch.empty_like(x)
+                        f = getattr(lib, "crvec_exp2_dev" if name == "exp2d" else "crvec_log_dev")
+                        assert f(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.c_size_t(n), m, s) == 0
+                        outs.append(y.view(torch.int64))
+                    torch.cuda.synchronize()
+                    d = int((outs[0] != outs[1]).sum())
+                    if d:
+                        print(f"{v} {name} mode {m}: {d} differing outputs", flush=True)
+                    bad += d
+        fns32 = [f for f in fns if f not in ("exp2d", "logd")]
+        for fn in fns32:
             for dist in ("config", "uniform", "bits"):
                 if dist == "bits":  # every bit pattern class: NaN payloads, Inf, zeros, subnormals
                     x = torch.randint(-2**31, 2**31, (n,), device="cuda", dtype=torch.int64).to(torch.int32).view(torch.float32)
