@@ -80,3 +80,15 @@ def test_corpus_replay_fp64(cuda, tmp_path):
     p = tmp_path / "exp2.txt"
     p.write_text("\n".join(v.hex() for v in hard_exp2()) + "\n")
     assert verify_cli.main(["corpus", "--fn", "exp2", "--file", str(p), "--all-modes"]) == 0
+
+
+@pytest.mark.parametrize("fn", ["expf", "logf", "log1pf", "sinf", "sincosf", "acosf", "rsqrtf"])
+def test_verify_cli_consistency(cuda, fn):
+    """SPEC consistency_check through the CLI: device vs host path, alignment /
+    split independence, array vs scalar entry point, oracle subset; all modes."""
+    assert verify_cli.main(["consistency", "--fn", fn, "--n", "300000", "--seed", "7"]) == 0
+
+
+def test_verify_cli_exactness_and_jobs(cuda):
+    assert verify_cli.main(["exactness"]) == 0
+    assert verify_cli.main(["verify", "--fn", "expm1f", "--mode", "rd", "--stride", "4096", "--jobs", "2"]) == 0

@@ -4,6 +4,12 @@ reference's proj/src/verify.cpp and tools/crvec.cpp are stubs).
   python tests/verify_cli.py verify   --fn expf --mode all [--stride 1] [--range LO:HI] [--report R.json]
   python tests/verify_cli.py corpus   --fn log  --file PATH [--all-modes]
   python tests/verify_cli.py callouts --fn log  --uniform 0.5:2.0 --n 10000000 [--seed S]
+  python tests/verify_cli.py consistency --fn expf --n 1000000 [--seed S]
+  python tests/verify_cli.py exactness
+
+--jobs N sets the host threads of the oracle comparisons (default: all cores);
+the GPU side needs none. Every command prints one JSON document (the
+VerifyReport schema above) and a one-line human summary on stderr.
 
 verify --stride 1 without a range runs the exhaustive 2^32 GPU sweep against
 the golden chunk hashes and re-checks any mismatching chunk element by element
@@ -51,13 +57,16 @@ def gpu_eval(name: str, xbits: np.ndarray, mode: int) -> np.ndarray:
     return out.cpu().numpy().view(np.uint32)
 
 
+JOBS = 0  # oracle threads (0 = all host cores)
+
+
 def compare(name, x, modes, report, cap=100):
     outs = [("sin", "cos")] if name == "sincosf" else [crvec.ORACLE_NAME[name]]
     for m in modes:
         got = gpu_eval(name, x, m)
         got = got if isinstance(got, tuple) else (got,)
         for g, ofn in zip(got, outs[0] if name == "sincosf" else outs):
-            want = O.f32(ofn, x, m)
+            want = O.f32(ofn, x, m, threads=JOBS)
             bad = np.nonzero(g != want)[0]
             report["mismatch_count"] += int(len(bad))
             for i in bad[: max(0, cap - len(report["mismatches"]))]:
@@ -159,6 +168,104 @@ def cmd_callouts(a):
     return 0
 
 
+def cmd_consistency(a):
+    """consistency_check (ref: SPEC.md verify module): for n seeded random lanes
+    (half uniform bit patterns, half the function's interesting range), the
+    device-pointer path equals the host-pointer path, array results equal the
+    scalar entry point lane by lane, results do not depend on the array's
+    alignment / length split (element offsets 1..3 take the scalar head and a
+    different vector phase), and a subset equals the oracle (the reference
+    backend here)."""
+    import torch
+    rng = np.random.default_rng(a.seed)
+    from tests.inputs import RANGES
+    lo, hi = RANGES[a.fn]
+    x = np.concatenate([rng.integers(0, 2 ** 32, a.n // 2, dtype=np.uint64).astype(np.uint32),
+                        rng.uniform(lo, hi, a.n - a.n // 2).astype(np.float32).view(np.uint32)])
+    rep = {"fn": a.fn, "n": int(a.n), "seed": a.seed, "checks": {}}
+    ok = True
+    for m in range(4):
+        xf = x.view(np.float32)
+        host = crvec.eval_f32(a.fn, xf, m)
+        dev = crvec.eval_f32(a.fn, torch.from_numpy(xf).cuda(), m)
+        host = host if isinstance(host, tuple) else (host,)
+        dev = dev if isinstance(dev, tuple) else (dev,)
+        same = all(np.array_equal(h.view(np.uint32), d.cpu().numpy().view(np.uint32)) for h, d in zip(host, dev))
+        rep["checks"][f"device_vs_host_mode{m}"] = same
+        ok &= same
+        # alignment / split independence: the same lanes at element offsets 1..3
+        for off in (1, 2, 3):
+            buf = torch.empty(a.n + off, dtype=torch.float32, device="cuda")
+            buf[off:] = torch.from_numpy(xf).cuda()
+            o = crvec.eval_f32(a.fn, buf[off:], m)
+            o = o if isinstance(o, tuple) else (o,)
+            same = all(np.array_equal(h.view(np.uint32), d.cpu().numpy().view(np.uint32)) for h, d in zip(host, o))
+            rep["checks"][f"offset{off}_mode{m}"] = same
+            ok &= same
+        # array vs scalar entry point (single-output functions)
+        if a.fn != "sincosf":
+            sc = getattr(crvec, "cr_" + a.fn + "_scalar")
+            idx = rng.integers(0, a.n, 64)
+            same = all(np.float32(sc(float(xf[i]), m)).view(np.uint32) == host[0].view(np.uint32)[i]
+                       or (np.isnan(xf[i]) and np.isnan(host[0][i])) for i in idx)
+            rep["checks"][f"array_vs_scalar_mode{m}"] = bool(same)
+            ok &= bool(same)
+        # subset vs the oracle
+        sub = x[:: max(1, a.n // 65536)]
+        outs = ("sin", "cos") if a.fn == "sincosf" else (crvec.ORACLE_NAME[a.fn],)
+        got = crvec.eval_f32(a.fn, sub.view(np.float32), m)
+        got = got if isinstance(got, tuple) else (got,)
+        same = all(np.array_equal(g.view(np.uint32), O.f32(f, sub, m, threads=JOBS)) for g, f in zip(got, outs))
+        rep["checks"][f"oracle_subset_mode{m}"] = same
+        ok &= same
+    rep["pass"] = bool(ok)
+    print(json.dumps(rep, indent=1))
+    return 0 if ok else 1
+
+
+def cmd_exactness(a):
+    """Exactness suite (ref: SPEC.md acceptance #5): algebraically exact
+    results in every mode — exp2f / exp2 on integers (normal and subnormal
+    powers of two), log2f on powers of two, log(1) = +0 — plus the other exact
+    cases the binary32 functions have (exp/expm1/sinh/tanh/sin/tan/asin/atan
+    of +-0, cos(0) = cosh(0) = 1, log/log10/log1p of 1 / 10^k / 0, rsqrt of
+    4^k), each compared with the oracle as well as with the exact value."""
+    rep = {"checks": {}, "fn": "all"}
+    ok = True
+    ints = np.arange(-149, 128, dtype=np.float32)
+    p2 = np.array([2.0 ** k for k in range(-149, 128)], dtype=np.float32)
+    p10 = np.array([10.0 ** k for k in range(0, 11)], dtype=np.float32)
+    p4 = np.array([4.0 ** k for k in range(-74, 64)], dtype=np.float32)
+    zeros = np.array([0.0, -0.0], dtype=np.float32)
+    for m in range(4):
+        c = {
+            "exp2f(int)": np.array_equal(crvec.cr_exp2f(ints, m), np.ldexp(np.float32(1), ints.astype(int))),
+            "log2f(2^k)": np.array_equal(crvec.cr_log2f(p2, m), np.arange(-149, 128, dtype=np.float32)),
+            "exp2(int)": np.array_equal(crvec.cr_exp2(np.arange(-1074, 1024, dtype=np.float64), m),
+                                        np.ldexp(1.0, np.arange(-1074, 1024))),
+            "log(1)=+0": bool(crvec.cr_log(np.array([1.0]), m)[0] == 0.0 and
+                              not np.signbit(crvec.cr_log(np.array([1.0]), m)[0])),
+            "log10f(10^k)": np.array_equal(crvec.cr_log10f(p10, m), np.arange(0, 11, dtype=np.float32)),
+            "rsqrtf(4^k)": np.array_equal(crvec.cr_rsqrtf(p4, m), (1.0 / np.sqrt(p4.astype(np.float64))).astype(np.float32)),
+            "cos/cosh(0)=1": bool((crvec.cr_cosf(zeros, m) == 1).all() and (crvec.cr_coshf(zeros, m) == 1).all()),
+        }
+        for name in ("expm1f", "sinhf", "tanhf", "sinf", "tanf", "asinf", "atanf", "log1pf"):
+            r = getattr(crvec, "cr_" + name)(zeros, m)
+            c[f"{name}(+-0)"] = bool(np.array_equal(r.view(np.uint32), zeros.view(np.uint32)))
+        for k, v in c.items():
+            rep["checks"][f"{k}_mode{m}"] = bool(v)
+            ok &= bool(v)
+        for name in crvec.F32_FUNCS:  # the same exact inputs through the oracle
+            xs = np.concatenate([ints, p2, p10, p4, zeros]).view(np.uint32)
+            got = crvec.eval_f32(name, xs.view(np.float32), m).view(np.uint32)
+            same = np.array_equal(got, O.f32(crvec.ORACLE_NAME[name], xs, m, threads=JOBS))
+            rep["checks"][f"{name}_oracle_mode{m}"] = same
+            ok &= same
+    rep["pass"] = bool(ok)
+    print(json.dumps(rep, indent=1))
+    return 0 if ok else 1
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="crvec")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -168,6 +275,7 @@ def main(argv=None):
     v.add_argument("--stride", type=int, default=1)
     v.add_argument("--range")
     v.add_argument("--report")
+    v.add_argument("--jobs", type=int, default=0, help="oracle host threads (0 = all cores)")
     c = sub.add_parser("corpus")
     c.add_argument("--fn", required=True)
     c.add_argument("--file", required=True)
@@ -177,8 +285,20 @@ def main(argv=None):
     k.add_argument("--uniform", required=True)
     k.add_argument("--n", type=int, default=10_000_000)
     k.add_argument("--seed", type=int, default=1)
+    q = sub.add_parser("consistency")
+    q.add_argument("--fn", required=True, choices=list(crvec.FN_IDS))
+    q.add_argument("--n", type=int, default=1_000_000)
+    q.add_argument("--seed", type=int, default=1)
+    sub.add_parser("exactness")
     a = ap.parse_args(argv)
-    return {"verify": cmd_verify, "corpus": cmd_corpus, "callouts": cmd_callouts}[a.cmd](a)
+    if not hasattr(a, "fn"):
+        a.fn = "all"
+    global JOBS
+    JOBS = getattr(a, "jobs", 0) or 0
+    rc = {"verify": cmd_verify, "corpus": cmd_corpus, "callouts": cmd_callouts,
+          "consistency": cmd_consistency, "exactness": cmd_exactness}[a.cmd](a)
+    print(f"crvec {a.cmd} --fn {a.fn}: {'PASS' if rc == 0 else 'FAIL'}", file=sys.stderr)
+    return rc
 
 
 if __name__ == "__main__":
