@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kT64) k_hardscan64(const double *x, uint64_t n
       V = logd_value(main ? xv : 2.0, 0, T).V;
     }
     if (main) {
-      const double d = boundary_rel_distance64(V);
+      const double d = boundary_rel_distance64(fast_two_sum(V.hi, V.lo));  // normalised pair
       if (d < thr) {
         const unsigned long long k = atomicAdd(count, 1ull);
         if (k < cap) {

@@ -366,14 +366,17 @@ CR_F Exp2dV exp2d_value(double xs, const F64Tab &T) {
   const Pair64 A = T.ta[ia], B = T.tb[ib];
   const double ah = A.a, alo = A.b, bh = B.a, blo = B.b;
   double Th = mul_(ah, bh);
-  double Tl = add_(fma_(ah, bh, -Th), fma_(ah, blo, mul_(alo, bh)));
+  double Tl = fma_(ah, blo, fma_(alo, bh, fma_(ah, bh, -Th)));  // inner fma exact
   double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
   DD lin = two_prod(R, LN2D_H);
   double pl = fma_(mul_(R, R), q, fma_(R, LN2D_L, lin.lo));
   DD aa = two_prod(Th, lin.hi);
   DD v = fast_two_sum(Th, aa.hi);
   double lo = add_(add_(v.lo, aa.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
-  return {fast_two_sum(v.hi, lo), N, k, R};
+  // (v.hi, lo) is left unnormalised (|lo| <= ~2 ulp(v.hi)): the round test
+  // rounds v.hi + (lo +- b) directly, and a final fast_two_sum (exact) would
+  // not change the enclosure
+  return {DD{v.hi, lo}, N, k, R};
 }
 
 // Rule-complete form (scalar kernels, the side-queue drain).
@@ -442,7 +445,7 @@ CR_F LogdV logd_value(double xs, int eadj, const F64Tab &T) {
   double tl = fma_(ed, LN2_LD, T.lll[i]);
   DD v = two_sum(th, a.hi);
   double lo = add_(add_(v.lo, tl), add_(fma_(-0.5, s.lo, a.lo), small));
-  const DD V = fast_two_sum(v.hi, lo);
+  const DD V = {v.hi, lo};  // unnormalised, as in exp2d_value
   return {V, fma_(dabs(small), 0x1p-49, EPS_LOGD * dabs(V.hi))};
 }
 

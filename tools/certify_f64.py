@@ -85,7 +85,7 @@ def certify_exp2(T, eps, rep):
             ah, alo, bh, blo = AH[ia], AL[ia], BH[ib], BL[ib]
             Th = ah * bh
             t1 = fma(ah, bh, -Th)  # exact product error
-            Tl = t1 + fma(ah, blo, alo * bh)
+            Tl = fma(ah, blo, fma(alo, bh, t1))  # the kernel's 3-FMA form
             exact = mp.power(2, mp.mpf(64 * ia + ib) / 4096)
             eT = max(eT, float(abs(mp.mpf(Th) + mp.mpf(Tl) - exact) / exact))
             tl_ratio = max(tl_ratio, abs(Tl) / Th)
