@@ -158,8 +158,12 @@ int crvec_round_test_f64(const double *hi, const double *lo, const int64_t *scal
  * for all four modes at once; for CRVEC_FN_SINCOSF, hashes2 receives the cos
  * outputs' hashes. hashes / hashes2 / counters are DEVICE pointers and must be
  * zeroed by the caller (the sweep accumulates). counters[0] += fast-path
- * lanes sent to the accurate path. force_accurate != 0 routes every non-
- * special lane through the accurate path (self-check of that path). */
+ * lanes sent to the accurate path. force_accurate: 0 = the sweep kernels'
+ * fast path + accurate fallback; 1 routes every non-special lane through the
+ * accurate path (self-check of that path); 3 runs the PRODUCT map kernels (the
+ * crvec_<fn>f_dev path, with its streaming template, rare-path form and
+ * shape) over the chunks' patterns in all four modes and hashes their outputs
+ * the same way (stream-ordered device workspace of 512-768 MiB). */
 int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *hashes,
                     uint64_t *hashes2, uint64_t *counters, int force_accurate, void *stream);
 

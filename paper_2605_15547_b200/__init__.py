@@ -250,9 +250,15 @@ def cr_log_scalar(x: float, mode=RoundingMode.NearestEven) -> float:
     return float(cr_log(np.array([x]), mode)[0])
 
 
-def sweep_f32(name: str, chunk_lo: int = 0, chunk_hi: int = 4096, force_accurate: bool = False,
+SWEEP_KERNELS, SWEEP_ACCURATE, SWEEP_MAP_KERNELS = 0, 1, 3  # crvec_sweep_f32 force modes
+
+
+def sweep_f32(name: str, chunk_lo: int = 0, chunk_hi: int = 4096, force_accurate: int = SWEEP_KERNELS,
               device=None):
     """Exhaustive sweep (C ABI crvec_sweep_f32) on the current CUDA device.
+    force_accurate: SWEEP_KERNELS (0), SWEEP_ACCURATE (1 / True: every
+    main-range lane through the accurate path) or SWEEP_MAP_KERNELS (3: the
+    product map kernels, crvec_<fn>f_dev, over every pattern, 4 modes).
 
     Returns (hashes[chunks, 4] uint64, hashes_cos or None, accurate_lanes)."""
     import torch

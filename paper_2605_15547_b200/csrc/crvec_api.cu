@@ -181,6 +181,56 @@ int host_pipeline(Dev *D, const T *x, T *y, T *y2, size_t n, Launch &&lf) {
   return CRVEC_OK;
 }
 
+// ---- map-kernel sweep (force mode 3): the PRODUCT map kernels over every
+// pattern of a chunk range, in all four modes, hashed like the sweep kernels
+// (the sweep kernels share the function code but not the streaming template,
+// the rare-path forms or the kernel shapes; this run covers those too).
+__global__ void k_iota(uint32_t *x, uint32_t first, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = first + i;
+}
+// one block per 4096 patterns (256 blocks per 2^20 chunk): h[chunk*4 + mode] +=
+// sum mix64((y << 32) | p)
+__global__ void __launch_bounds__(crvec::kThreads) k_hash_chunks(const uint32_t *y, uint32_t first,
+                                                                 uint64_t *h, int mode) {
+  const uint32_t i0 = blockIdx.x * (uint32_t)crvec::kSweepPerBlock;
+  uint64_t acc[1] = {0};
+  for (int j = 0; j < crvec::kSweepPerThread; ++j) {
+    const uint32_t i = i0 + j * crvec::kThreads + threadIdx.x;
+    acc[0] += crvec::mix64(((uint64_t)y[i] << 32) | (uint64_t)(first + i));
+  }
+  crvec::block_add<1>(acc, h + 4ull * (blockIdx.x / crvec::kSweepBlocksPerChunk) + mode);
+}
+
+int map_sweep(Dev *D, int fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *h, uint64_t *h2,
+              cudaStream_t s) {
+  constexpr uint32_t kBlockChunks = 64;  // 2^26 patterns (256 MiB) per pass
+  const uint32_t cap = kBlockChunks << 20;
+  uint32_t *x = nullptr, *y = nullptr, *y2 = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&x, 4ull * cap, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&y, 4ull * cap, s);
+  if (e == cudaSuccess && h2) e = cudaMallocAsync((void **)&y2, 4ull * cap, s);
+  int rc = e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
+  for (uint32_t c = chunk_lo; rc == CRVEC_OK && c < chunk_hi; c += kBlockChunks) {
+    const uint32_t nc = chunk_hi - c < kBlockChunks ? chunk_hi - c : kBlockChunks;
+    const uint32_t n = nc << 20, first = c << 20;
+    k_iota<<<1184, 256, 0, s>>>(x, first, n);
+    for (int m = 0; m < 4 && rc == CRVEC_OK; ++m) {
+      rc = launch(D, fn, (const float *)x, (float *)y, (float *)y2, n, m, s);
+      if (rc) break;
+      const unsigned blocks = nc * crvec::kSweepBlocksPerChunk;
+      k_hash_chunks<<<blocks, crvec::kThreads, 0, s>>>(y, first, h + 4ull * (c - chunk_lo), m);
+      if (h2) k_hash_chunks<<<blocks, crvec::kThreads, 0, s>>>(y2, first, h2 + 4ull * (c - chunk_lo), m);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) rc = cuda_fail(e);
+    }
+  }
+  if (x) cudaFreeAsync(x, s);
+  if (y) cudaFreeAsync(y, s);
+  if (y2) cudaFreeAsync(y2, s);
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -370,6 +420,9 @@ int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_
   Dev *D;
   int rc = device(&D);
   if (rc) return rc;
+  if (force_accurate == 3)
+    return map_sweep(D, fn, chunk_lo, chunk_hi, hashes, fn == CRVEC_FN_SINCOSF ? hashes2 : nullptr,
+                     (cudaStream_t)stream);
   cudaError_t e = g_table[fn].sweep(chunk_lo, chunk_hi, hashes, hashes2, force_accurate,
                                     (cudaStream_t)stream, (unsigned long long *)counters);
   return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);

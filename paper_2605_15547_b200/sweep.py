@@ -70,11 +70,15 @@ def rows_for(names: Sequence[str]) -> List[str]:
 
 
 def run_device(names: Sequence[str], rank: int = 0, world: int = 1, chunks: int = CHUNKS,
-               force_accurate: bool = False, reduce: bool = True, stream=None):
+               force_accurate: int = 0, reduce: bool = True, stream=None):
     """Device-resident sweep (the GPU path bench.py times): every function's
     chunk hashes are accumulated by the crvec_sweep_f32 kernels straight into
     one zeroed [rows, chunks, 4] int64 tensor on this rank's GPU (no host round
     trip, no per-function synchronisation), then ONE all_reduce(sum) over NCCL.
+
+    force_accurate: 0 = the sweep kernels (fast path + accurate fallback),
+    1 = every main-range lane through the accurate path, 3 = the product map
+    kernels (crvec_<fn>f_dev) over every pattern in all four modes.
 
     Returns (rows, table tensor on the device, accurate-lane counter tensor).
     The caller copies the table to the host once, after its timing events."""

@@ -133,6 +133,22 @@ def test_exhaustive_sweep_vs_golden(cuda, name):
     assert len(bad) == 0, f"{name}: {len(bad)} chunks differ, first {bad[:10]}"
 
 
+@pytest.mark.parametrize("name", crvec.F32_FUNCS + ["sincosf"])
+def test_map_kernels_exhaustive_vs_golden(cuda, name):
+    """The PRODUCT map kernels (crvec_<fn>f_dev: streaming template, rare-path
+    form, kernel shape) over all 2^32 inputs x 4 modes, hashed per 2^20 chunk
+    like the sweep: equal to the oracle's golden (sweep force mode 3)."""
+    h, h2, _ = crvec.sweep_f32(name, force_accurate=crvec.SWEEP_MAP_KERNELS)
+    if name == "sincosf":
+        gs, gc = _golden("sin"), _golden("cos")
+        assert (h == gs).all(), f"sin chunks differ: {np.nonzero((h != gs).any(1))[0][:10]}"
+        assert (h2 == gc).all(), f"cos chunks differ: {np.nonzero((h2 != gc).any(1))[0][:10]}"
+        return
+    g = _golden(crvec.ORACLE_NAME[name])
+    bad = np.nonzero((h != g).any(1))[0]
+    assert len(bad) == 0, f"{name}: {len(bad)} chunks differ, first {bad[:10]}"
+
+
 @pytest.mark.parametrize("name", crvec.F32_FUNCS)
 def test_accurate_path_self_check(cuda, name):
     """Route EVERY non-special lane through the double-double accurate path
