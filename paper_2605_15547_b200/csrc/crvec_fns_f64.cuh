@@ -370,13 +370,14 @@ CR_F Exp2dV exp2d_value(double xs, const F64Tab &T) {
   double q = fma_(fma_(fma_(EXP2D_Q4[3], R, EXP2D_Q4[2]), R, EXP2D_Q4[1]), R, EXP2D_Q4[0]);
   DD lin = two_prod(R, LN2D_H);
   double pl = fma_(mul_(R, R), q, fma_(R, LN2D_L, lin.lo));
-  DD aa = two_prod(Th, lin.hi);
-  DD v = fast_two_sum(Th, aa.hi);
-  double lo = add_(add_(v.lo, aa.lo), fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
-  // (v.hi, lo) is left unnormalised (|lo| <= ~2 ulp(v.hi)): the round test
-  // rounds v.hi + (lo +- b) directly, and a final fast_two_sum (exact) would
-  // not change the enclosure
-  return {DD{v.hi, lo}, N, k, R};
+  // s = RN(Th + Th ph) in one FMA; its rounding error e1 = (Th + Th ph) - s by
+  // a second FMA over Th - s (exact: s lies within a factor 2 of Th), e1 itself
+  // rounded once (~2^-106 |V|). (s, lo) is left unnormalised (|lo| <= ~ulp(s)):
+  // the round test rounds s + (lo +- b) directly.
+  const double s = fma_(Th, lin.hi, Th);
+  const double e1 = fma_(Th, lin.hi, sub_(Th, s));
+  const double lo = add_(e1, fma_(Th, pl, fma_(Tl, lin.hi, Tl)));
+  return {DD{s, lo}, N, k, R};
 }
 
 // Rule-complete form (scalar kernels, the side-queue drain).

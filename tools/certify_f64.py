@@ -116,7 +116,8 @@ def certify_exp2(T, eps, rep):
     pmin = -Rm * H - plmax
     dp_rel = epl / (1 + pmin)
     rep.append(f"exp2 (a3) roundings in p: |dp| <= 2^{lg2(epl):.1f}, relative to V 2^{lg2(dp_rel):.1f}")
-    # (a4) assembly V = Th + Th ph + [Tl + Th pl + Tl ph] (v, aa exact; Tl pl neglected)
+    # (a4) assembly V = s + e1 + [Th pl + Tl ph + Tl] with s = RN(Th + Th ph) (one FMA),
+    # e1 = RN(Th ph + (Th - s)) its rounding error (Th - s exact, Sterbenz), Tl pl neglected
     Tlm = tl_ratio * Tmax
     lin_hi = Rm * H
     neg = Tlm * plmax                                       # Tl * pl dropped
@@ -124,15 +125,13 @@ def certify_exp2(T, eps, rep):
     e_t2 = U * t2m
     t3m = Tmax * plmax + t2m
     e_t3 = U * t3m + Tmax * 0 + e_t2                        # + propagated t2 error
-    vlo = U * Tmax * (1 + lin_hi) * 2                       # |v.lo| <= ulp(v.hi)/2, v.hi < 2 Tmax
-    aalo = U * Tmax * lin_hi
-    s1m = vlo + aalo
-    e_s1 = U * s1m
-    e_lo = U * (s1m + t3m)
+    e1m = U * Tmax * (1 + lin_hi) * 2                       # |e1| <= ulp(s)/2, s < 2 Tmax
+    e_e1 = U * e1m                                          # e1 rounded once
+    e_lo = U * (e1m + t3m)                                  # lo = RN(e1 + t3)
     Vmin = Tmin * (1 + pmin)
-    e_asm = (neg + e_t3 + e_s1 + e_lo) / Vmin
-    rep.append(f"exp2 (a4) assembly: Tl pl 2^{lg2(neg):.1f}, t3 2^{lg2(U * t3m):.1f}, lo 2^{lg2(e_lo):.1f}; "
-               f"relative to V >= {Vmin:.6f}: 2^{lg2(e_asm):.1f}")
+    e_asm = (neg + e_t3 + e_e1 + e_lo) / Vmin
+    rep.append(f"exp2 (a4) assembly: Tl pl 2^{lg2(neg):.1f}, t3 2^{lg2(U * t3m):.1f}, e1 2^{lg2(e_e1):.1f}, "
+               f"lo 2^{lg2(e_lo):.1f}; relative to V >= {Vmin:.6f}: 2^{lg2(e_asm):.1f}")
     total = float((1 + mp.mpf(eT)) * (1 + mp.mpf(eapx)) * (1 + mp.mpf(dp_rel)) * (1 + mp.mpf(e_asm)) - 1)
     ok = total < eps
     rep.append(f"exp2 TOTAL a-priori relative bound 2^{lg2(total):.2f} vs EPS_EXP2D = 2^{lg2(eps):.0f}: "
