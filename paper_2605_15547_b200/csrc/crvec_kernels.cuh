@@ -321,8 +321,11 @@ __device__ __forceinline__ PHBlock *ph_storage() {
 // Rare-path form per function (measured, profiles/r01/ab_rare_store.txt,
 // profiles/r01/tune_store_form.txt, profiles/r01/tune_vw8.txt):
 // store form (resolve after the vector store, scalar overwrite) or register
-// form (gather + scatter before the store). The choice changes the main
-// path's register allocation, so it is taken per kernel.
+// form (gather + scatter before the store); within the store form, the staged
+// variant (RareStaged above: shared-memory row + per-lane loop, round 2,
+// profiles/r02/ab_log_rare.txt, ab_other.txt) for the log family, tanh, sinh.
+// The choice changes the main path's register allocation, so it is taken per
+// kernel; shapes re-measured in round 2 (log1pf, expm1f 8:2:2).
 template <class F> struct RareStore { static constexpr bool value = false; };
 template <int B> struct RareStore<FnLogB<B>> { static constexpr bool value = true; };
 template <bool A> struct RareStore<FnAsinAcos<A>> { static constexpr bool value = true; };
