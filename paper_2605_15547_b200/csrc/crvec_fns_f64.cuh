@@ -439,7 +439,12 @@ CR_F LogdV logd_value(double xs, int eadj, const F64Tab &T) {
   const double *P = LOGD5_P;
   double p = fma_(fma_(fma_(fma_(fma_(fma_(P[6], r, P[5]), r, P[4]), r, P[3]), r, P[2]), r, P[1]), r, P[0]);
   double small = mul_(mul_(r, s.hi), p);          // r^3 P(r)
-  DD a = fast_two_sum(r, -0.5 * s.hi);            // |r| > |r^2/2|
+  // a = r - r^2/2 exactly as a pair: a.hi = RN(r - s.hi/2) by one FMA, a.lo
+  // its rounding error by a second FMA over r - a.hi (exact: a.hi is within a
+  // factor 2 of r); the error of RN(r - s.hi/2) is representable, so exact
+  DD a;
+  a.hi = fma_(-0.5, s.hi, r);
+  a.lo = fma_(-0.5, s.hi, sub_(r, a.hi));
   // e ln2 + L: the high parts add exactly (both on the 2^-40 grid)
   double ed = i2d(e);
   double th = fma_(ed, LN2_HD, cl.b);
@@ -471,8 +476,8 @@ CR_F F64Out logd_special(double x, const F64Tab &T) {
 
 template <int M>
 CR_F F64Out logd_main_path(double x, const F64Tab &T) {
-  const uint64_t xb = d2u(x);
-  const bool ok = xb - 0x0010000000000000ull < 0x7FE0000000000000ull && x != 1.0;  // positive normal
+  // positive normal (high word in [0x00100000, 0x7FF00000)) and x != 1
+  const bool ok = (uint32_t)d2hi(x) - 0x00100000u < 0x7FE00000u && x != 1.0;
   F64Out r = logd_core<M>(ok ? x : 2.0, 0, T);
   r.decided = r.decided && ok;
   return r;
