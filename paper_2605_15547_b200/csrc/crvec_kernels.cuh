@@ -627,6 +627,27 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z;
 }
 
+// Per-mode chunk-hash terms mix64((y_m << 32) | p) of one pattern, with two
+// mix64 evaluations instead of four: correctly rounded results in the four
+// modes take at most two values, RD's and RU's (RZ is one of them, RN is one
+// of them), so RN and RZ reuse those hashes. Any other value (never, for
+// correct outputs) is still hashed exactly by the fallback branch, so the sum
+// stays the definition's whatever the outputs are.
+__device__ __forceinline__ void hash4(const uint32_t (&y)[4], uint32_t p, uint64_t *acc) {
+  const uint64_t hd = mix64(((uint64_t)y[RD] << 32) | p);
+  const uint64_t hu = mix64(((uint64_t)y[RU] << 32) | p);
+  uint64_t hn = y[RNE] == y[RD] ? hd : hu;
+  uint64_t hz = y[RZ] == y[RD] ? hd : hu;
+  if ((y[RNE] != y[RD] && y[RNE] != y[RU]) || (y[RZ] != y[RD] && y[RZ] != y[RU])) {
+    hn = mix64(((uint64_t)y[RNE] << 32) | p);
+    hz = mix64(((uint64_t)y[RZ] << 32) | p);
+  }
+  acc[RNE] += hn;
+  acc[RZ] += hz;
+  acc[RU] += hu;
+  acc[RD] += hd;
+}
+
 template <class F>
 __device__ __forceinline__ void finish4(float x, Fast f, uint32_t (&y)[4], bool &fail) {
   if constexpr (HasTinyRule<F>::value) {
@@ -714,8 +735,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(uint32_t chunk_lo, uint64_t 
         round4(slow_dd<F>(xs[e]), y);
         ++nslow;
       }
-#pragma unroll
-      for (int m = 0; m < 4; ++m) acc[m] += mix64(((uint64_t)y[m] << 32) | xb);
+      hash4(y, xb, acc);
     }
   }
   if (nslow) atomicAdd(counters, (unsigned long long)nslow);
@@ -759,11 +779,8 @@ __global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, ui
       finish4<FnCos>(xs[e], b, yc, fc);
       if (fs || (FORCE && a.main)) { round4(slow_dd<FnSin>(xs[e]), ys); ++nslow; }
       if (fc || (FORCE && b.main)) { round4(slow_dd<FnCos>(xs[e]), yc); ++nslow; }
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        acc[m] += mix64(((uint64_t)ys[m] << 32) | xb);
-        acc[4 + m] += mix64(((uint64_t)yc[m] << 32) | xb);
-      }
+      hash4(ys, xb, acc);
+      hash4(yc, xb, acc + 4);
     }
   }
   if (nslow) atomicAdd(counters, (unsigned long long)nslow);
