@@ -703,8 +703,8 @@ __device__ __forceinline__ void block_add(uint64_t (&acc)[K], uint64_t *dst) {
 // Exhaustive sweep over binary32 patterns: each block covers 4096 patterns of
 // one 2^20 chunk (256 blocks per chunk); every pattern is evaluated once and
 // converted in all four modes; per chunk and mode the hashes are summed.
-constexpr int kSweepPerThread = 16;
-constexpr int kSweepPerBlock = kThreads * kSweepPerThread;  // 4096
+constexpr int kSweepPerThread = 64;
+constexpr int kSweepPerBlock = kThreads * kSweepPerThread;  // 16384 (64 per thread: 0.348 -> 0.323 s, tools/sweep_time.py)
 constexpr int kSweepBlocksPerChunk = (1 << 20) / kSweepPerBlock;
 
 template <class F, bool FORCE>
