@@ -163,7 +163,9 @@ int crvec_round_test_f64(const double *hi, const double *lo, const int64_t *scal
  * accurate path (self-check of that path); 3 runs the PRODUCT map kernels (the
  * crvec_<fn>f_dev path, with its streaming template, rare-path form and
  * shape) over the chunks' patterns in all four modes and hashes their outputs
- * the same way (stream-ordered device workspace of 512-768 MiB). */
+ * the same way (stream-ordered device workspace of 512-768 MiB); 4 does the
+ * same with relatively misaligned input / output arrays, i.e. through the
+ * element kernel that serves unaligned calls. */
 int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *hashes,
                     uint64_t *hashes2, uint64_t *counters, int force_accurate, void *stream);
 

@@ -250,15 +250,17 @@ def cr_log_scalar(x: float, mode=RoundingMode.NearestEven) -> float:
     return float(cr_log(np.array([x]), mode)[0])
 
 
-SWEEP_KERNELS, SWEEP_ACCURATE, SWEEP_MAP_KERNELS = 0, 1, 3  # crvec_sweep_f32 force modes
+SWEEP_KERNELS, SWEEP_ACCURATE, SWEEP_MAP_KERNELS, SWEEP_ELEMENT_KERNELS = 0, 1, 3, 4  # crvec_sweep_f32 modes
 
 
 def sweep_f32(name: str, chunk_lo: int = 0, chunk_hi: int = 4096, force_accurate: int = SWEEP_KERNELS,
               device=None):
     """Exhaustive sweep (C ABI crvec_sweep_f32) on the current CUDA device.
     force_accurate: SWEEP_KERNELS (0), SWEEP_ACCURATE (1 / True: every
-    main-range lane through the accurate path) or SWEEP_MAP_KERNELS (3: the
-    product map kernels, crvec_<fn>f_dev, over every pattern, 4 modes).
+    main-range lane through the accurate path), SWEEP_MAP_KERNELS (3: the
+    product map kernels, crvec_<fn>f_dev, over every pattern, 4 modes) or
+    SWEEP_ELEMENT_KERNELS (4: the same through the element kernel that serves
+    relatively misaligned arrays).
 
     Returns (hashes[chunks, 4] uint64, hashes_cos or None, accurate_lanes)."""
     import torch

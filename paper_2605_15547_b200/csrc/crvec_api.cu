@@ -202,12 +202,16 @@ __global__ void __launch_bounds__(crvec::kThreads) k_hash_chunks(const uint32_t 
   crvec::block_add<1>(acc, h + 4ull * (blockIdx.x / crvec::kSweepBlocksPerChunk) + mode);
 }
 
+// misaligned = true: the input sits one float past a 256-byte boundary and
+// the outputs on one, so the arrays are relatively misaligned and the whole
+// range runs the element kernel (k_map_scalar) instead of the vector kernel.
 int map_sweep(Dev *D, int fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *h, uint64_t *h2,
-              cudaStream_t s) {
+              cudaStream_t s, bool misaligned = false) {
   constexpr uint32_t kBlockChunks = 64;  // 2^26 patterns (256 MiB) per pass
   const uint32_t cap = kBlockChunks << 20;
-  uint32_t *x = nullptr, *y = nullptr, *y2 = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&x, 4ull * cap, s);
+  uint32_t *xbuf = nullptr, *y = nullptr, *y2 = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&xbuf, 4ull * cap + 256, s);
+  uint32_t *x = xbuf + (misaligned ? 1 : 0);
   if (e == cudaSuccess) e = cudaMallocAsync((void **)&y, 4ull * cap, s);
   if (e == cudaSuccess && h2) e = cudaMallocAsync((void **)&y2, 4ull * cap, s);
   int rc = e == cudaSuccess ? CRVEC_OK : cuda_fail(e);
@@ -225,7 +229,7 @@ int map_sweep(Dev *D, int fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_t *h,
       if (e != cudaSuccess) rc = cuda_fail(e);
     }
   }
-  if (x) cudaFreeAsync(x, s);
+  if (xbuf) cudaFreeAsync(xbuf, s);
   if (y) cudaFreeAsync(y, s);
   if (y2) cudaFreeAsync(y2, s);
   return rc;
@@ -420,9 +424,9 @@ int crvec_sweep_f32(crvec_fn_t fn, uint32_t chunk_lo, uint32_t chunk_hi, uint64_
   Dev *D;
   int rc = device(&D);
   if (rc) return rc;
-  if (force_accurate == 3)
+  if (force_accurate == 3 || force_accurate == 4)
     return map_sweep(D, fn, chunk_lo, chunk_hi, hashes, fn == CRVEC_FN_SINCOSF ? hashes2 : nullptr,
-                     (cudaStream_t)stream);
+                     (cudaStream_t)stream, force_accurate == 4);
   cudaError_t e = g_table[fn].sweep(chunk_lo, chunk_hi, hashes, hashes2, force_accurate,
                                     (cudaStream_t)stream, (unsigned long long *)counters);
   return e == cudaSuccess ? CRVEC_OK : cuda_fail(e);

@@ -149,6 +149,20 @@ def test_map_kernels_exhaustive_vs_golden(cuda, name):
     assert len(bad) == 0, f"{name}: {len(bad)} chunks differ, first {bad[:10]}"
 
 
+@pytest.mark.parametrize("name", crvec.F32_FUNCS + ["sincosf"])
+def test_element_kernels_exhaustive_vs_golden(cuda, name):
+    """The element kernel (k_map_scalar: relatively misaligned arrays, one
+    element per lane, register-form rare path) over all 2^32 inputs x 4 modes:
+    equal to the golden (sweep mode 4)."""
+    h, h2, _ = crvec.sweep_f32(name, force_accurate=crvec.SWEEP_ELEMENT_KERNELS)
+    if name == "sincosf":
+        assert (h == _golden("sin")).all() and (h2 == _golden("cos")).all()
+        return
+    g = _golden(crvec.ORACLE_NAME[name])
+    bad = np.nonzero((h != g).any(1))[0]
+    assert len(bad) == 0, f"{name}: {len(bad)} chunks differ, first {bad[:10]}"
+
+
 @pytest.mark.parametrize("name", crvec.F32_FUNCS)
 def test_accurate_path_self_check(cuda, name):
     """Route EVERY non-special lane through the double-double accurate path
