@@ -1,7 +1,7 @@
 """Developer soak test: binary64 exp2 / log on the GPU vs the CPU oracle over
 2^N random inputs per range (paper range, wide range, random bit patterns) in
 all four modes. Prints mismatch counts and the fast-path undecided rate.
-usage: python tools/soak_f64.py [log2n=23]"""
+usage: python tools/soak_f64.py [log2n=23] [seed=2026]"""
 import os
 import sys
 import time
@@ -17,7 +17,8 @@ from oracle import oracle as O  # noqa: E402
 def main():
     import torch
     n = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 23)
-    rng = np.random.default_rng(2026)
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2026
+    rng = np.random.default_rng(seed)
     sets = {
         "exp2": [rng.uniform(-20, 20, n), rng.uniform(-1075, 1024, n // 4),
                  rng.integers(0, 2 ** 64, n // 4, dtype=np.uint64).view(np.float64)],
