@@ -398,7 +398,7 @@ struct FnTanh {
 template <int TAG>
 CR_F const D2 *log_pairs(const double *L) {
 #if CR_DEVICE
-  __shared__ D2 tab[16];
+  __shared__ __align__(256) D2 tab[16];  // 256-aligned: see log_pair()
   if (threadIdx.x < 16) tab[threadIdx.x] = D2{hilo2d(LOG_C_HI[threadIdx.x], 0u), L[threadIdx.x]};
   __syncthreads();
   return tab;
@@ -406,6 +406,21 @@ CR_F const D2 *log_pairs(const double *L) {
   static D2 tab[16];
   for (int i = 0; i < 16; ++i) tab[i] = D2{hilo2d(LOG_C_HI[i], 0u), L[i]};
   return tab;
+#endif
+}
+
+// Entry (i & 15) of a log_pairs table for the raw bin index i = hh >> 16:
+// byte offset (hh >> 12) & 0xF0 OR-ed into the 256-aligned shared address
+// (SHF + one 3-input LOP3, then LDS.128 [R]; the indexed C++ form adds the
+// table base with an extra IADD per element).
+CR_F D2 log_pair(const D2 *t, int hh) {
+#if CR_DEVICE
+  const uint32_t a = (((uint32_t)hh >> 12) & 0xF0u) | (uint32_t)__cvta_generic_to_shared(t);
+  D2 r;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+  return r;
+#else
+  return t[(hh >> 16) & 15];
 #endif
 }
 
@@ -443,7 +458,7 @@ CR_F const D2 *sh_table16(const double *A, const double *B, const int *W) {
 // offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
 // relative-accurate); r = m*c_i - 1 (exact when m has <= 24 bits).
 struct RedLog {
-  int e, i;
+  int e, i, hh;
   double m;
 };
 // `i` is the raw bin index (bits above the 16-bin field included): table
@@ -452,7 +467,7 @@ CR_F RedLog red_log(double xd) {
   int h = d2hi(xd);
   int hh = h - 0x3FE88000;
   int e = hh >> 20;
-  return {e, hh >> 16, hilo2d(h - (int)((uint32_t)e << 20), d2lo(xd))};
+  return {e, hh >> 16, hh, hilo2d(h - (int)((uint32_t)e << 20), d2lo(xd))};
 }
 
 template <int BASE>  // 0: ln, 2: log2, 10: log10
@@ -465,7 +480,7 @@ struct FnLogB {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     RedLog q = red_log(f2d(x));
-    const D2 cl = R.t[q.i & 15];
+    const D2 cl = log_pair(R.t, q.hh);
     const double c = cl.x, L = cl.y;
     double r = fma_(q.m, c, -1.0);  // exact
     double p = fma_(mul_(r, r), logq(r), r);
@@ -478,6 +493,8 @@ struct FnLogB {
     return Fast{a, in_main(xb)};
   }
   CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < +Inf
+  // the map kernels test main as kMainLo < x <= FLT_MAX (float compares)
+  static constexpr float kMainLo = 0.0f;
   // branch-free: +-0 -> -Inf, +Inf -> +Inf, NaN -> quiet(x), x < 0 -> qNaN
   template <int M>
   CR_F static uint32_t special(float x) {
@@ -515,38 +532,46 @@ struct FnLog1p {
     uint32_t xb = f2u(x);
     double y = add_(1.0, f2d(x));
     RedLog q = red_log(y);
-    const D2 cl = R.t[q.i & 15];
+    const D2 cl = log_pair(R.t, q.hh);
     const double c = cl.x, L = cl.y;
     double r = fma_(q.m, c, -1.0);
     double p = fma_(mul_(r, r), logq(r), r);
     double a = add_(fma_(i2d(q.e), LN2_D, L), p);
-    // main: 0 < |x| < inf and x > -1. Tiny |x| (the kernels apply tiny_bits)
-    return Fast{a, in_main(xb)};
+    // fast-path main: -1 < x < +Inf (two float compares; NaN fails both).
+    // +-0 is "main" here only because the tiny rule (which the kernels apply
+    // to every tiny lane, zeros included) returns it exactly; in_main() below
+    // keeps the zeros on the rule path for the rare / accurate routing.
+    (void)xb;
+    const bool main = (x > -1.0f) & (x <= 0x1.fffffep127f);
+    return Fast{a, main};
   }
   // |x| <= 2^-26 is ~40% of all bit patterns (79% of the config-2 mix): its
   // rule stays on the main path, applied to the result bits after the
   // conversion. log1p(x) = x - x^2/2 + ... lies strictly below x and within
   // x^2/2 < 2^-27 |x| of it, so in mode M it rounds to x (RNE, RU), to the
   // float below x (RD), or toward zero from there (RZ): an integer +-1.
+  // log1p(+-0) = +-0 exactly in every mode: the zeros are tiny and keep xb.
   static constexpr bool kTinyRule = true;
-  CR_F static bool is_tiny(uint32_t xb) { return (xb << 1) <= 0x65000000u; }
+  static constexpr float kTiny = 0x1p-26f;  // the map kernels' tiny test: |x| <= kTiny
+  static constexpr float kMainLo = -1.0f;   // map kernels: -1 < x <= FLT_MAX
+  CR_F static bool is_tiny(uint32_t xb) { return (xb << 1) <= 0x65000000u; }  // = |x| <= 2^-26
   template <int M>
   CR_F static uint32_t tiny_bits(uint32_t xb) {
     if (M == RNE || M == RU) return xb;
-    if (M == RZ) return (int)xb < 0 ? xb : xb - 1u;  // positive: the float below x
-    return (int)xb < 0 ? xb + 1u : xb - 1u;          // RD: next float toward -Inf
+    if (M == RZ) return (int)xb > 0 ? xb - 1u : xb;  // positive: the float below x
+    // RD: next float toward -Inf (x > 0: down; x < 0: magnitude up; zeros kept)
+    return (int)xb > 0 ? xb - 1u : (xb > 0x80000000u ? xb + 1u : xb);
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 2u, 0xFF000000u) && xb < 0xBF800000u; }
   template <int M>
   CR_F static uint32_t special(float x) {
-    uint32_t xb = f2u(x), az = xb << 1;
-    if (nan_bits(xb)) return quiet_bits(xb);
-    if (az == 0) return xb;
-    if (xb == 0xBF800000u) return 0xFF800000u;  // log1p(-1) = -Inf
-    if (xb > 0xBF800000u) return 0x7FC00000u;   // x < -1
-    if (xb == 0x7F800000u) return 0x7F800000u;
-    double xd = f2d(x);
-    return f2u(cvt_f32<M>(fma_(-dabs(xd), 0x1p-36, xd)));  // x - x^2/2 just below x
+    // branch-free (the rare loop runs it divergently): the tiny rule, then
+    // +Inf, x <= -1 and NaN by selects
+    const uint32_t xb = f2u(x);
+    uint32_t r = tiny_bits<M>(xb);                                  // +-0 and |x| <= 2^-26
+    r = xb == 0x7F800000u ? xb : r;                                 // +Inf
+    r = xb >= 0xBF800000u ? (xb == 0xBF800000u ? 0xFF800000u : 0x7FC00000u) : r;  // x <= -1
+    return nan_bits(xb) ? quiet_bits(xb) : r;
   }
   CR_F static DD slow(float x) {
     double xd = f2d(x);

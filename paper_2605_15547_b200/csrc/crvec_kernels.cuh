@@ -168,6 +168,11 @@ struct HasTinyRule { static constexpr bool value = false; };
 template <class F>
 struct HasTinyRule<F, decltype((void)F::kTinyRule)> { static constexpr bool value = F::kTinyRule; };
 
+template <class F, class = void>
+struct HasFloatMain { static constexpr bool value = false; };
+template <class F>
+struct HasFloatMain<F, decltype((void)F::kMainLo)> { static constexpr bool value = true; };
+
 // Common path for NE elements per lane: fast approximation, one static-mode
 // conversion, and the per-lane mask of rare slots (bit e: slot e is outside
 // the main range, or undecided by the rounding test).
@@ -181,14 +186,43 @@ __device__ __forceinline__ unsigned fast_eval(const float (&xs)[NE], uint32_t (&
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     ys[e] = f2u(cvt_f32<M>(f[e].a));
-    bool rare = (!f[e].main) | near_boundary(f[e].a, F::E);
-    if constexpr (HasTinyRule<F>::value) {  // log1pf: tiny-argument rule on the result bits
-      const uint32_t xb = f2u(xs[e]);
-      const bool tiny = F::is_tiny(xb);
-      ys[e] = tiny ? F::template tiny_bits<M>(xb) : ys[e];
-      rare = rare & !(tiny & f[e].main);
+    if constexpr (HasFloatMain<F>::value) {
+      // Log family: the rare bit as one predicate chain and one predicated OR
+      // (the bool form compiles to 3-5 SEL per element): undecided by the
+      // rounding test, or x outside (kMainLo, FLT_MAX] (unordered compares:
+      // NaN is rare), and for log1pf not tiny (the tiny rule, zeros included,
+      // is applied to the result bits below).
+      constexpr uint32_t W = 0x0FFFFFFFu & ~(4u * F::E - 1u);
+      if constexpr (HasTinyRule<F>::value) {
+        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t.reg .f32 a;\n\t"
+            "add.u32 t, %1, %4;\n\t"
+            "and.b32 t, t, %5;\n\t"
+            "setp.eq.u32 p, t, 0;\n\t"
+            "setp.leu.or.f32 p, %2, %6, p;\n\t"
+            "setp.gtu.or.f32 p, %2, 0f7F7FFFFF, p;\n\t"
+            "abs.f32 a, %2;\n\t"
+            "setp.gtu.and.f32 p, a, %7, p;\n\t"
+            "@p or.b32 %0, %0, %3;\n\t}"
+            : "+r"(mask)
+            : "r"(d2lo(f[e].a)), "f"(xs[e]), "r"(1u << e), "n"(2u * F::E), "n"(W),
+              "f"(F::kMainLo), "f"(F::kTiny));
+      } else {
+        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+            "add.u32 t, %1, %4;\n\t"
+            "and.b32 t, t, %5;\n\t"
+            "setp.eq.u32 p, t, 0;\n\t"
+            "setp.leu.or.f32 p, %2, %6, p;\n\t"
+            "setp.gtu.or.f32 p, %2, 0f7F7FFFFF, p;\n\t"
+            "@p or.b32 %0, %0, %3;\n\t}"
+            : "+r"(mask)
+            : "r"(d2lo(f[e].a)), "f"(xs[e]), "r"(1u << e), "n"(2u * F::E), "n"(W), "f"(F::kMainLo));
+      }
+      if constexpr (HasTinyRule<F>::value)  // log1pf: tiny-argument rule on the result bits
+        ys[e] = fabsf(xs[e]) <= F::kTiny ? F::template tiny_bits<M>(f2u(xs[e])) : ys[e];
+    } else {
+      bool rare = (!f[e].main) | near_boundary(f[e].a, F::E);
+      mask |= (unsigned)rare << e;
     }
-    mask |= (unsigned)rare << e;
   }
   return mask;
 }
@@ -270,11 +304,13 @@ __device__ __forceinline__ void resolve_rare_staged(const float (&xs)[NE], unsig
 #pragma unroll
     for (int k = 0; k < NE / 4; ++k) row[k] = make_float4(xs[4 * k], xs[4 * k + 1], xs[4 * k + 2], xs[4 * k + 3]);
     const float *rf = reinterpret_cast<const float *>(row);
+    float *yl = yf + fbase;  // the lane's first output float: one 64-bit add per step
     int cnt = 0;
     do {
-      const uint32_t e = (uint32_t)__ffs(mask) - 1u;
-      yf[fbase + (32u * VW * (e / VW) + (e % VW))] = u2f(resolve_one<F, M>(rf[e], cnt));
-      mask &= mask - 1u;
+      // highest pending slot first: one FLO (no bit reverse), 32-bit offsets
+      const uint32_t e = 31u - (uint32_t)__clz((int)mask);
+      yl[32u * VW * (e / VW) + (e % VW)] = u2f(resolve_one<F, M>(rf[e], cnt));
+      mask ^= 1u << e;
     } while (mask);
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);
   }
@@ -824,7 +860,7 @@ __global__ void __launch_bounds__(kThreads) k_hardscan(uint32_t chunk_lo, double
     Fast f;
     if constexpr (IsTrig<F>::value) f = F::from_red(x, RedTrig{0, 0.0}, R);  // only .main is used
     else f = F::fast(x, R);
-    if (f.main) {  // divergent body without shuffles; fast() above runs converged
+    if (f.main && F::in_main(xb)) {  // divergent body without shuffles; fast() above runs converged
       double d = boundary_rel_distance(slow_dd<F>(x));
       if (d < thr) {
         unsigned long long k = atomicAdd(count, 1ull);
