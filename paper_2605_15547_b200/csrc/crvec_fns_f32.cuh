@@ -133,6 +133,9 @@ struct FnExp {
     return Fast{exp_core3(q.k, q.r, R.t), in_main(f2u(x))};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x65000002u, 0xFF000000u); }
+  // map kernels: main <=> 2^-26 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-26f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -157,6 +160,9 @@ struct FnExp2 {
     return Fast{exp_core3((int)d2lo(t), mul_(u, LN2_D), R.t), in_main(f2u(x))};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x65000002u, 0xFF000000u); }
+  // map kernels: main <=> 2^-26 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-26f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -185,6 +191,9 @@ struct FnExp10 {
     return Fast{exp_core3((int)d2lo(t), r, R.t), in_main(f2u(x))};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x63000002u, 0xFF000000u); }
+  // map kernels: main <=> 2^-28 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-28f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) { return exp_like_special<M>(f2u(x)); }
   CR_F static DD slow(float x) {
@@ -311,6 +320,9 @@ struct FnSinh {
     return Fast{with_sign(fma_(h.Sa, h.cr, mul_(h.Ca, h.sr)), xb), in_main(xb)};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000000u); }  // 2^-12 < |x| < inf
+  // map kernels: main <=> 2^-12 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-12f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -336,6 +348,9 @@ struct FnCosh {
     return Fast{fma_(h.Ca, h.cr, mul_(h.Sa, h.sr)), in_main(f2u(x))};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x72000002u, 0xFF000000u); }  // 2^-13 < |x| < inf
+  // map kernels: main <=> 2^-13 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-13f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
@@ -399,6 +414,10 @@ template <int TAG>
 CR_F const D2 *log_pairs(const double *L) {
 #if CR_DEVICE
   __shared__ __align__(256) D2 tab[16];  // 256-aligned: see log_pair()
+  // The user shared window starts after a reserved region, so the alignment
+  // of the shared *address* is checked, not assumed (a misplaced table would
+  // otherwise read wrong rows silently).
+  if (((uint32_t)__cvta_generic_to_shared(tab) & 255u) != 0u) __trap();
   if (threadIdx.x < 16) tab[threadIdx.x] = D2{hilo2d(LOG_C_HI[threadIdx.x], 0u), L[threadIdx.x]};
   __syncthreads();
   return tab;
@@ -493,8 +512,9 @@ struct FnLogB {
     return Fast{a, in_main(xb)};
   }
   CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < +Inf
-  // the map kernels test main as kMainLo < x <= FLT_MAX (float compares)
-  static constexpr float kMainLo = 0.0f;
+  // map kernels: main <=> 0 < x <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = false;
+  static constexpr float kMainLo = 0.0f, kMainHi = 0x1.fffffep127f;
   // branch-free: +-0 -> -Inf, +Inf -> +Inf, NaN -> quiet(x), x < 0 -> qNaN
   template <int M>
   CR_F static uint32_t special(float x) {
@@ -551,9 +571,9 @@ struct FnLog1p {
   // x^2/2 < 2^-27 |x| of it, so in mode M it rounds to x (RNE, RU), to the
   // float below x (RD), or toward zero from there (RZ): an integer +-1.
   // log1p(+-0) = +-0 exactly in every mode: the zeros are tiny and keep xb.
-  static constexpr bool kTinyRule = true;
   static constexpr float kTiny = 0x1p-26f;  // the map kernels' tiny test: |x| <= kTiny
-  static constexpr float kMainLo = -1.0f;   // map kernels: -1 < x <= FLT_MAX
+  static constexpr bool kMainAbs = false;   // map kernels: -1 < x <= FLT_MAX
+  static constexpr float kMainLo = -1.0f, kMainHi = 0x1.fffffep127f;
   CR_F static bool is_tiny(uint32_t xb) { return (xb << 1) <= 0x65000000u; }  // = |x| <= 2^-26
   template <int M>
   CR_F static uint32_t tiny_bits(uint32_t xb) {
@@ -693,42 +713,34 @@ CR_F DD red_trig_dd(float x, int &k) {
   return r;
 }
 
-// Big-argument lanes of a warp are reduced together (warp-cooperative
-// Payne-Hanek): see coop_payne_hanek() in the kernel file. This helper is the
-// per-lane body it runs, in binary64 arithmetic on the exponent-indexed table
-// PH_T (tools/gen_tables.py gen_ph_table: x * T_j = M * C_j, the bits of
-// 16/pi that matter for this exponent, exact for j < 3):
-//   k0 = RN(x T0), f0 = x T0 - k0 (exact), k1 = RN(f0 + x T1),
-//   s = (f0 - k1) + x T1 (exact, |s| <= 1/2: 53-bit grid), s += x T2 (exact
-//   while |s| < 2^-28), s += x T3; k = k0 + k1
-// x*16/pi has at most ~30 leading zero fraction bits for a binary32 x, so r
-// keeps ~2^-52 relative accuracy (the fast path's budget is 2^-43).
-#ifndef CRVEC_PH_INT
-CR_F RedTrig ph_reduce(float x, const D2 *tab) {
-  const uint32_t xb = f2u(x);
-  const int row = (int)((xb >> 23) & 0xFFu) - 139;  // 2^12 <= |x| < Inf: 0 .. 115
-  const D2 a = tab[2 * row], b = tab[2 * row + 1];
-  const double xd = f2d(x);
-  const double t = fma_(xd, a.x, SHIFTER);
-  const double kd = sub_(t, SHIFTER);
-  const double f0 = fma_(xd, a.x, -kd);                 // exact, |f0| <= 1/2
-  const double t1 = add_(fma_(xd, a.y, f0), SHIFTER);   // k1 = RN(f0 + x T1)
-  double s = fma_(xd, a.y, sub_(f0, sub_(t1, SHIFTER)));  // exact, |s| <= 1/2
-  s = fma_(xd, b.x, s);
-  s = fma_(xd, b.y, s);
-  return {(int)(d2lo(t) + d2lo(t1)), mul_(s, PI_16_RN)};
-}
+// Exponent-indexed Payne-Hanek reduction (the fast path of every lane of a
+// warp step that holds a large argument; tools/gen_tables.py gen_ph_table):
+// x = M 2^E, row b = biased exponent holds hi + lo = (16/pi) mod 2^(5-E) with
+// |x (hi + lo - T_E)| < 2^-77 and hi short enough that f0 = x hi - RN(x hi)
+// is exact; then u = f0 + x lo in one FMA (relative 2^-53) and r = u pi/16.
+// k = RN(x hi) (mod 32 from the shifter's low word). x*16/pi has at most ~30
+// leading zero fraction bits for a binary32 x, so r keeps > 2^-46 relative
+// accuracy (the fast path's budget is 2^-44); |u| <= 1/2 + 2^-24.
+// Row address: the table's shared address + (b << 4).
+CR_F D2 ph_row(const D2 *tab, uint32_t xb) {
+#if CR_DEVICE
+  const uint32_t a = ((xb >> 19) & 0xFF0u) + (uint32_t)__cvta_generic_to_shared(tab);
+  D2 r;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+  return r;
 #else
-CR_F RedTrig ph_reduce(float x, const unsigned *words) {
-  uint32_t xb = f2u(x);
-  PH p = payne_hanek<4>(xb & 0x7FFFFFFFu, words);
-  double fr = fma_((double)(p.f2 >> 11), 0x1p-53, (double)p.f);
-  double r = mul_(fr, PI_16_2M64_H);
-  int k = p.k;
-  if (xb >> 31) { k = -k; r = -r; }
-  return {k, r};
-}
+  return tab[(xb >> 23) & 0xFFu];
 #endif
+}
+CR_F RedTrig red_trig_ph(float x, const D2 *tab) {
+  const D2 h = ph_row(tab, f2u(x));
+  const double xd = f2d(x);
+  const double t = fma_(xd, h.x, SHIFTER);
+  const double kd = sub_(t, SHIFTER);
+  const double f0 = fma_(xd, h.x, -kd);  // exact, |f0| <= 1/2
+  const double u = fma_(xd, h.y, f0);
+  return {(int)d2lo(t), mul_(u, PI_16_RN)};
+}
 
 // One 16-entry shared table of (sin(j pi/16), cos(j pi/16)) pairs, j = k mod
 // 16, read with one LDS.128 (5-8% faster than two register tables read with
@@ -739,7 +751,6 @@ CR_F double flip_k16(double v, int k) { return hilo2d(d2hi(v) ^ ((k << 27) & (in
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
   static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
-  static constexpr bool kBigArg = true;
   struct Regs { const D2 *t; };
   CR_F static void load(Regs &R) { R.t = sh_table16<100, false>(SIN16_HI, COS16_HI, nullptr); }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
@@ -757,6 +768,9 @@ struct FnTrig {
   CR_F static bool in_main(uint32_t xb) {
     return in_range(xb << 1, WHICH == 0 ? 0x73000002u : 0x72000002u, 0xFF000000u);
   }
+  // map kernels: main <=> 2^-12 (sin) / 2^-13 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = WHICH == 0 ? 0x1p-12f : 0x1p-13f, kMainHi = 0x1.fffffep127f;
   // sin and cos from one reduction and one table read.
   CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
     double s = mul_(q.r, q.r);
@@ -766,10 +780,6 @@ struct FnTrig {
     const uint32_t xb = f2u(x);
     fs = Fast{flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k), FnTrig<0>::in_main(xb)};
     fc = Fast{flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k), FnTrig<1>::in_main(xb)};
-  }
-  CR_F static bool is_big(float x) {
-    uint32_t az = f2u(x) << 1;
-    return az >= (0x45800000u << 1) && az < 0xFF000000u;  // 2^12 <= |x| < inf
   }
   template <int M>
   CR_F static uint32_t special(float x) {
@@ -861,6 +871,9 @@ struct FnAtan {
     return Fast{with_sign(add_(A, atan_t2(t)), xb), in_main(xb)};
   }
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000002u); }  // 2^-12 < |x| <= inf
+  // map kernels: main <=> 2^-12 < |x| <= +Inf (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-12f, kMainHi = __builtin_huge_valf();
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
@@ -923,6 +936,9 @@ struct FnAsinAcos {
   CR_F static bool in_main(uint32_t xb) {
     return ACOS ? (xb << 1) < 0x7F000000u : in_range(xb << 1, 0x73000002u, 0x7F000000u);
   }
+  // map kernels: main <=> (acos: any, asin: 2^-12 <) |x| < 1 (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = ACOS ? -1.0f : 0x1p-12f, kMainHi = 0x1.fffffep-1f;
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);
@@ -968,6 +984,9 @@ struct FnRsqrt {
     return Fast{newton(f2d(x)), in_main(f2u(x))};
   }
   CR_F static bool in_main(uint32_t xb) { return xb - 1u < 0x7F7FFFFFu; }  // 0 < x < inf
+  // map kernels: main <=> 0 < x <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = false;
+  static constexpr float kMainLo = 0.0f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x);

@@ -87,57 +87,33 @@ __device__ __noinline__ DD slow_dd(float x) {
   return F::slow(x);
 }
 
-// ---------------------------------------------- warp-cooperative Payne-Hanek
-// Per-warp staging: the big-argument elements of the warp's 32 x NE slots are
-// compacted (one ballot per slot: slot-major queue positions) into a shared
-// queue, reduced 32 at a time by all lanes, and read back by their owners.
-// One pass serves up to 32 big arguments however they are spread over lanes
-// and slots.
-struct PHWarp {
-  double rr[256];
-  int qx[256];  // queued x bits, overwritten by the reduced k
-};
+// ------------------------------------------------ trig argument reduction
+// Warp-uniform Payne-Hanek: while no lane of the warp's step holds a large
+// argument (|x| >= 2^12) every lane takes the two-part Cody-Waite reduction;
+// as soon as one does, the whole warp takes the exponent-indexed Payne-Hanek
+// reduction (red_trig_ph: the bits of 16/pi that matter for x's exponent,
+// one 16-byte shared-table row, 4 FP64 operations + the pi/16 scaling),
+// which is exact for small arguments too. No compaction, no queue, no
+// divergence: round 1's per-warp ballot queue cost ~25 thread-instructions
+// per element on the config-3 mix (profiles/r02/ncu_lines_sinf.txt).
 struct PHBlock {
-#ifndef CRVEC_PH_INT
-  D2 tab[232];  // PH_T
-#else
-  unsigned tab[12];
-#endif
-  PHWarp warp[kWarps];
+  D2 tab[256];  // PH_T rows by biased exponent
 };
 
 template <int NE>
-__device__ __forceinline__ void coop_payne_hanek(const float (&xs)[NE], const bool (&big)[NE],
-                                                 RedTrig (&q)[NE], PHBlock &sh) {
-  static_assert(32 * NE <= 256, "PHWarp holds 32 x 8 queued arguments");
-  const int lane = threadIdx.x & 31;
-  PHWarp &w = sh.warp[threadIdx.x >> 5];
-  const unsigned lt = (1u << lane) - 1u;
-  // slot-major queue: one ballot per slot gives each big element its position
-  int pos[NE];
-  int total = 0;
+__device__ __forceinline__ void trig_reduce(const float (&xs)[NE], RedTrig (&q)[NE], const PHBlock *sh) {
+#ifndef CRVEC_TRIG_UNIFIED
+  float mx = 0.0f;  // NaN lanes are ignored by fmaxf (they are rare lanes either way)
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const unsigned b = __ballot_sync(kFull, big[e]);
-    pos[e] = total + __popc(b & lt);
-    total += __popc(b);
-    if (big[e]) w.qx[pos[e]] = (int)f2u(xs[e]);
-  }
-  __syncwarp();
-  // all lanes reduce the compacted queue, 32 arguments per pass
-  for (int b0 = 0; b0 < total; b0 += 32) {
-    int i = b0 + lane;
-    if (i < total) {
-      RedTrig r = ph_reduce(u2f((uint32_t)w.qx[i]), sh.tab);
-      w.qx[i] = r.k;
-      w.rr[i] = r.r;
-    }
-  }
-  __syncwarp();
+  for (int e = 0; e < NE; ++e) mx = fmaxf(mx, fabsf(xs[e]));
+  if (!__any_sync(kFull, mx >= 0x1p12f)) {
 #pragma unroll
-  for (int e = 0; e < NE; ++e)
-    if (big[e]) q[e] = RedTrig{w.qx[pos[e]], w.rr[pos[e]]};
-  __syncwarp();
+    for (int e = 0; e < NE; ++e) q[e] = red_trig_small(f2d(xs[e]));
+    return;
+  }
+#endif
+#pragma unroll
+  for (int e = 0; e < NE; ++e) q[e] = red_trig_ph(xs[e], sh->tab);
 }
 
 // Fast results for NE elements per lane (warp converged on entry).
@@ -146,15 +122,7 @@ __device__ __forceinline__ void fast_lanes(const float (&xs)[NE], Fast (&f)[NE],
                                            const typename F::Regs &R, PHBlock *sh) {
   if constexpr (IsTrig<F>::value) {
     RedTrig q[NE];
-    bool big[NE];
-    bool any = false;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      q[e] = red_trig_small(f2d(xs[e]));
-      big[e] = F::is_big(xs[e]);
-      any |= big[e];
-    }
-    if (__any_sync(kFull, any)) coop_payne_hanek<NE>(xs, big, q, *sh);
+    trig_reduce<NE>(xs, q, sh);
 #pragma unroll
     for (int e = 0; e < NE; ++e) f[e] = F::from_red(xs[e], q[e], R);
   } else {
@@ -163,15 +131,54 @@ __device__ __forceinline__ void fast_lanes(const float (&xs)[NE], Fast (&f)[NE],
   }
 }
 
+
+// Rare bit of one slot, OR-ed into `mask` with one predicated OR: the lane is
+// undecided by the rounding test (near_boundary on the low word of `a`) or x
+// is outside the function's main range kLo < v <= kHi, v = |x| (kMainAbs) or
+// x, tested with unordered float compares so NaN is rare; functions with a
+// tiny rule also drop tiny lanes (|x| <= kTiny, the rule is applied to the
+// result bits). One predicate chain: VIADD, LOP3.P, 2-3 FSETP, predicated
+// VIADD (the bool form, (!main | nb) << e, compiles to 2-5 SEL per element).
+// The float range is the same set as F::in_main (integer form, used by the
+// rare path and the sweep kernels); the exhaustive map-kernel sweep checks it.
 template <class F, class = void>
-struct HasTinyRule { static constexpr bool value = false; };
+struct HasTiny { static constexpr bool value = false; };
 template <class F>
-struct HasTinyRule<F, decltype((void)F::kTinyRule)> { static constexpr bool value = F::kTinyRule; };
+struct HasTiny<F, decltype((void)F::kTiny)> { static constexpr bool value = true; };
 
 template <class F, class = void>
-struct HasFloatMain { static constexpr bool value = false; };
+struct HasMainRange { static constexpr bool value = false; };
 template <class F>
-struct HasFloatMain<F, decltype((void)F::kMainLo)> { static constexpr bool value = true; };
+struct HasMainRange<F, decltype((void)F::kMainAbs)> { static constexpr bool value = true; };
+
+template <class F>
+__device__ __forceinline__ void rare_or(unsigned &mask, double a, float x, unsigned bit) {
+  constexpr uint32_t W = 0x0FFFFFFFu & ~(4u * F::E - 1u);
+  const float v = F::kMainAbs ? fabsf(x) : x;
+  if constexpr (HasTiny<F>::value) {
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "add.u32 t, %1, %4;\n\t"
+        "and.b32 t, t, %5;\n\t"
+        "setp.eq.u32 p, t, 0;\n\t"
+        "setp.leu.or.f32 p, %2, %6, p;\n\t"
+        "setp.gtu.or.f32 p, %2, %7, p;\n\t"
+        "setp.gtu.and.f32 p, %8, %9, p;\n\t"
+        "@p or.b32 %0, %0, %3;\n\t}"
+        : "+r"(mask)
+        : "r"(d2lo(a)), "f"(v), "r"(bit), "n"(2u * F::E), "n"(W), "f"(F::kMainLo), "f"(F::kMainHi),
+          "f"(fabsf(x)), "f"(F::kTiny));
+  } else {
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "add.u32 t, %1, %4;\n\t"
+        "and.b32 t, t, %5;\n\t"
+        "setp.eq.u32 p, t, 0;\n\t"
+        "setp.leu.or.f32 p, %2, %6, p;\n\t"
+        "setp.gtu.or.f32 p, %2, %7, p;\n\t"
+        "@p or.b32 %0, %0, %3;\n\t}"
+        : "+r"(mask)
+        : "r"(d2lo(a)), "f"(v), "r"(bit), "n"(2u * F::E), "n"(W), "f"(F::kMainLo), "f"(F::kMainHi));
+  }
+}
 
 // Common path for NE elements per lane: fast approximation, one static-mode
 // conversion, and the per-lane mask of rare slots (bit e: slot e is outside
@@ -186,43 +193,14 @@ __device__ __forceinline__ unsigned fast_eval(const float (&xs)[NE], uint32_t (&
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     ys[e] = f2u(cvt_f32<M>(f[e].a));
-    if constexpr (HasFloatMain<F>::value) {
-      // Log family: the rare bit as one predicate chain and one predicated OR
-      // (the bool form compiles to 3-5 SEL per element): undecided by the
-      // rounding test, or x outside (kMainLo, FLT_MAX] (unordered compares:
-      // NaN is rare), and for log1pf not tiny (the tiny rule, zeros included,
-      // is applied to the result bits below).
-      constexpr uint32_t W = 0x0FFFFFFFu & ~(4u * F::E - 1u);
-      if constexpr (HasTinyRule<F>::value) {
-        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t.reg .f32 a;\n\t"
-            "add.u32 t, %1, %4;\n\t"
-            "and.b32 t, t, %5;\n\t"
-            "setp.eq.u32 p, t, 0;\n\t"
-            "setp.leu.or.f32 p, %2, %6, p;\n\t"
-            "setp.gtu.or.f32 p, %2, 0f7F7FFFFF, p;\n\t"
-            "abs.f32 a, %2;\n\t"
-            "setp.gtu.and.f32 p, a, %7, p;\n\t"
-            "@p or.b32 %0, %0, %3;\n\t}"
-            : "+r"(mask)
-            : "r"(d2lo(f[e].a)), "f"(xs[e]), "r"(1u << e), "n"(2u * F::E), "n"(W),
-              "f"(F::kMainLo), "f"(F::kTiny));
-      } else {
-        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
-            "add.u32 t, %1, %4;\n\t"
-            "and.b32 t, t, %5;\n\t"
-            "setp.eq.u32 p, t, 0;\n\t"
-            "setp.leu.or.f32 p, %2, %6, p;\n\t"
-            "setp.gtu.or.f32 p, %2, 0f7F7FFFFF, p;\n\t"
-            "@p or.b32 %0, %0, %3;\n\t}"
-            : "+r"(mask)
-            : "r"(d2lo(f[e].a)), "f"(xs[e]), "r"(1u << e), "n"(2u * F::E), "n"(W), "f"(F::kMainLo));
-      }
-      if constexpr (HasTinyRule<F>::value)  // log1pf: tiny-argument rule on the result bits
-        ys[e] = fabsf(xs[e]) <= F::kTiny ? F::template tiny_bits<M>(f2u(xs[e])) : ys[e];
-    } else {
-      bool rare = (!f[e].main) | near_boundary(f[e].a, F::E);
+    if constexpr (HasMainRange<F>::value) {
+      rare_or<F>(mask, f[e].a, xs[e], 1u << e);
+    } else {  // bool form (measured faster for expm1f / tanhf: register allocation)
+      const bool rare = (!f[e].main) | near_boundary(f[e].a, F::E);
       mask |= (unsigned)rare << e;
     }
+    if constexpr (HasTiny<F>::value)  // log1pf: tiny-argument rule on the result bits
+      ys[e] = fabsf(xs[e]) <= F::kTiny ? F::template tiny_bits<M>(f2u(xs[e])) : ys[e];
   }
   return mask;
 }
@@ -329,16 +307,12 @@ __device__ __forceinline__ void eval_lanes(const float (&xs)[NE], uint32_t (&ys)
   if (__any_sync(kFull, mask != 0)) resolve_rare<F, M, NE>(xs, ys, mask, counters);
 }
 
-// Shared staging exists only in the trig kernels (24 KB per block).
+// The Payne-Hanek table exists only in the trig kernels (4 KB per block).
 template <class F>
 __device__ __forceinline__ PHBlock *ph_storage() {
   if constexpr (IsTrig<F>::value) {
     __shared__ PHBlock sh;
-#ifndef CRVEC_PH_INT
-    for (int i = threadIdx.x; i < 232; i += blockDim.x) sh.tab[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
-#else
-    if (threadIdx.x < 12) sh.tab[threadIdx.x] = INV_PI_WORDS[threadIdx.x];
-#endif
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.tab[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
     __syncthreads();
     return &sh;
   } else {
@@ -497,15 +471,7 @@ __device__ __forceinline__ unsigned sincos_lanes(const float (&xs)[NE], uint32_t
                                                  PHBlock *sh, unsigned long long *counters) {
   static_assert(NE <= 16, "mask layout");
   RedTrig q[NE];
-  bool big[NE];
-  bool anyb = false;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    q[e] = red_trig_small(f2d(xs[e]));
-    big[e] = FnSin::is_big(xs[e]);
-    anyb |= big[e];
-  }
-  if (__any_sync(kFull, anyb)) coop_payne_hanek<NE>(xs, big, q, *sh);
+  trig_reduce<NE>(xs, q, sh);
   unsigned mask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
@@ -513,8 +479,8 @@ __device__ __forceinline__ unsigned sincos_lanes(const float (&xs)[NE], uint32_t
     FnSin::sincos_from_red(xs[e], q[e], R, a, b);
     s[e] = f2u(cvt_f32<M>(a.a));
     c[e] = f2u(cvt_f32<M>(b.a));
-    mask |= (unsigned)((!a.main) | near_boundary(a.a, FnSin::E)) << e;
-    mask |= (unsigned)((!b.main) | near_boundary(b.a, FnCos::E)) << (e + 16);
+    rare_or<FnSin>(mask, a.a, xs[e], 1u << e);
+    rare_or<FnCos>(mask, b.a, xs[e], 1u << (e + 16));
   }
   if (STORE_FORM) return mask;
   if (__any_sync(kFull, mask != 0)) {
@@ -686,7 +652,7 @@ __device__ __forceinline__ void hash4(const uint32_t (&y)[4], uint32_t p, uint64
 
 template <class F>
 __device__ __forceinline__ void finish4(float x, Fast f, uint32_t (&y)[4], bool &fail) {
-  if constexpr (HasTinyRule<F>::value) {
+  if constexpr (HasTiny<F>::value) {
     const uint32_t xb = f2u(x);
     if (f.main && F::is_tiny(xb)) {  // the map kernels' result-bits rule
       fail = false;
@@ -794,16 +760,9 @@ __global__ void __launch_bounds__(kThreads) k_sweep_sincos(uint32_t chunk_lo, ui
     uint32_t pb = p0 + it * (kThreads * 4) + threadIdx.x * 4;
     float xs[4];
     RedTrig q[4];
-    bool big[4];
-    bool anyb = false;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      xs[e] = u2f(pb + e);
-      q[e] = red_trig_small(f2d(xs[e]));
-      big[e] = FnSin::is_big(xs[e]);
-      anyb |= big[e];
-    }
-    if (__any_sync(kFull, anyb)) coop_payne_hanek<4>(xs, big, q, *sh);
+    for (int e = 0; e < 4; ++e) xs[e] = u2f(pb + e);
+    trig_reduce<4>(xs, q, sh);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t xb = pb + e;

@@ -217,32 +217,34 @@ def gen_log():
 
 # ----------------------------------------------------------------- trig ----
 def gen_ph_table():
-    """Exponent-indexed Payne-Hanek table for the fast path, |x| >= 2^12.
+    """Exponent-indexed Payne-Hanek table of the fast path (every binary32
+    exponent, so one reduction serves small and large arguments alike).
 
-    x = M * 2^(ex-23) (M < 2^24 an integer): x*16/pi mod 32 = M*C mod 32 with
-    C = (2^(ex-23) * 16/pi) mod 32 -- bits of C of weight >= 32 only add
-    multiples of 32*M. C is cut at 2^-24, 2^-53, 2^-82 into C0 (bits 2^4 ..
-    2^-24, <= 29 bits), C1, C2 (29 bits each) and C3 = RN(rest); the table
-    stores T_j = C_j * 2^-(ex-23), so x * T_j = M * C_j is exact in binary64
-    for j < 3. Row b - 139 for biased exponents b = 139 .. 254."""
-    emit("// Payne-Hanek fast-path table: 4 doubles per binary32 exponent 139..254")
+    x = M * 2^E (M < 2^24 an integer, E = max(b, 1) - 150 for biased exponent
+    b). x*16/pi mod 32 = x * T_E mod 32 with T_E = (16/pi) mod 2^(5-E): the
+    bits of 16/pi of weight >= 2^(5-E) only add multiples of 32*M. T_E is cut
+    into hi (lsb 2^-L, L = 48 + E for E > 2, min(50, 53 + E) otherwise: hi has
+    <= 53 bits and x*hi - RN(x*hi) is exact in binary64) and lo = RN(T_E - hi),
+    so |x * (hi + lo - T_E)| < 2^-77. Row b (16 bytes: hi, lo) for b = 0..255
+    (row 255, Inf/NaN, is never used on the main path)."""
+    emit("// Payne-Hanek fast-path table: (hi, lo) of (16/pi) mod 2^(5-E) per binary32 exponent")
     rows = []
     with mp.workprec(1200):
-        pi = mp.pi
-        for b in range(139, 255):
-            sc = mp.mpf(2) ** (b - 127 - 23)
-            c = sc * 16 / pi
-            c = c - 32 * mp.floor(c / 32)
-            parts = []
-            for cut in (24, 53, 82):
-                q = mp.floor(c * mp.mpf(2) ** cut) / mp.mpf(2) ** cut
-                parts.append(q)
-                c -= q
-            parts.append(c)
-            t = [d(q / sc) for q in parts[:3]] + [d(parts[3] / sc)]
-            for j in range(3):  # exact: C_j has <= 29 bits, the scale is a power of two
-                assert mp.mpf(t[j]) * sc == parts[j]
-            rows.extend(t)
+        C = 16 / mp.pi
+        for b in range(256):
+            if b == 255:
+                rows.extend([0.0, 0.0])
+                continue
+            E = max(b, 1) - 150
+            T = C - mp.mpf(2) ** (5 - E) * mp.floor(C / mp.mpf(2) ** (5 - E)) if E > 2 else C
+            L = 48 + E if E > 2 else min(50, 53 + E)
+            hi = mp.floor(T * mp.mpf(2) ** L) / mp.mpf(2) ** L
+            assert mp.mpf(d(hi)) == hi, b  # <= 53 bits
+            lo = d(T - hi)
+            rows.extend([d(hi), lo])
+            # |x (hi + lo - T)| for the largest x of this exponent
+            err = abs(mp.mpf(2) ** (E + 24) * (hi + mp.mpf(lo) - T))
+            assert err < mp.mpf(2) ** -76, (b, float(mp.log(err, 2)))
     arr("PH_T", rows)
 
 
