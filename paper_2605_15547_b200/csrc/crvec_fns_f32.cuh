@@ -443,35 +443,76 @@ CR_F D2 log_pair(const D2 *t, int hh) {
 #endif
 }
 
-// Generic shared 16-entry table: entry i = {A[i], B[i]} (+ optional third
-// value hilo2d(W[i], 0) at +16 B: 32-byte entries), same fill rule as above.
-template <int TAG, bool THIRD>
-CR_F const D2 *sh_table16(const double *A, const double *B, const int *W) {
+// Interleaved shared 16-entry pair table {A[i], B[i]} (one LDS.128 per
+// lookup; used where the column-split form measured slower: tanf).
+template <int TAG>
+CR_F const D2 *sh_pair16(const double *A, const double *B) {
 #if CR_DEVICE
-  __shared__ D2 tab[THIRD ? 32 : 16];
-  if (threadIdx.x < 16) {
-    if (THIRD) {
-      tab[2 * threadIdx.x] = D2{A[threadIdx.x], B[threadIdx.x]};
-      tab[2 * threadIdx.x + 1] = D2{hilo2d(W[threadIdx.x], 0u), 0.0};
-    } else {
-      tab[threadIdx.x] = D2{A[threadIdx.x], B[threadIdx.x]};
-    }
-  }
+  __shared__ __align__(16) D2 tab[16];
+  if (threadIdx.x < 16) tab[threadIdx.x] = D2{A[threadIdx.x], B[threadIdx.x]};
   __syncthreads();
-  return tab;
 #else
-  static D2 tab[THIRD ? 32 : 16];
-  for (int i = 0; i < 16; ++i) {
-    if (THIRD) {
-      tab[2 * i] = D2{A[i], B[i]};
-      tab[2 * i + 1] = D2{hilo2d(W[i], 0u), 0.0};
-    } else {
-      tab[i] = D2{A[i], B[i]};
-    }
-  }
+  static D2 tab[16];
+  for (int i = 0; i < 16; ++i) tab[i] = D2{A[i], B[i]};
+#endif
   return tab;
+}
+
+// Column-split shared 16-entry tables: NC columns of 16 doubles (128 bytes
+// each, one column per value). A warp's LDS.64 moves 256 bytes in two
+// 128-byte wavefronts and a column spans each bank exactly once, so any mix
+// of rows is conflict-free; the interleaved 16-byte-pair form (LDS.128)
+// conflicts whenever two lanes of a quarter-warp read rows r and r + 8
+// (ncu: 6.7 wavefronts per LDS.128 instead of 4 in sinf, round 2). Column c
+// of row j: base + 128 c + 8 (j & 15), one address per row and immediate
+// column offsets. W gives a third column as hilo2d(W[i], 0).
+template <int TAG, int NC>
+CR_F const double *sh_split16(const double *A, const double *B, const int *W) {
+#if CR_DEVICE
+  __shared__ __align__(16) double tab[16 * NC];
+#else
+  static double tab[16 * NC];
+#endif
+#if CR_DEVICE
+  if (threadIdx.x < 16) {
+    const int i = threadIdx.x;
+#else
+  for (int i = 0; i < 16; ++i) {
+#endif
+    tab[i] = A[i];
+    if (NC > 1) tab[16 + i] = B[i];
+    if (NC > 2) tab[32 + i] = hilo2d(W[i], 0u);
+  }
+#if CR_DEVICE
+  __syncthreads();
+#endif
+  return tab;
+}
+struct SplitRow {
+#if CR_DEVICE
+  uint32_t a;  // shared address of column 0, row j
+#else
+  const double *p;
+#endif
+};
+CR_F SplitRow split_row(const double *t, int j) {
+#if CR_DEVICE
+  return {(uint32_t)__cvta_generic_to_shared(t) + ((uint32_t)(j & 15) << 3)};
+#else
+  return {t + (j & 15)};
 #endif
 }
+template <int COL>
+CR_F double split_get(SplitRow r) {
+#if CR_DEVICE
+  double v;
+  asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(r.a), "n"(COL * 128));
+  return v;
+#else
+  return r.p[16 * COL];
+#endif
+}
+
 
 // x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window
 // offset (16 bins, 1.0 at the centre of bin 7 with c_7 = 1 so log near 1 is
@@ -722,17 +763,20 @@ CR_F DD red_trig_dd(float x, int &k) {
 // leading zero fraction bits for a binary32 x, so r keeps > 2^-46 relative
 // accuracy (the fast path's budget is 2^-44); |u| <= 1/2 + 2^-24.
 // Row address: the table's shared address + (b << 4).
-CR_F D2 ph_row(const D2 *tab, uint32_t xb) {
+// The table is column-split (hi[256] then lo[256], two LDS.64: exponents of
+// neighbouring lanes map to distinct banks, see sh_split16).
+CR_F D2 ph_row(const double *tab, uint32_t xb) {
 #if CR_DEVICE
-  const uint32_t a = ((xb >> 19) & 0xFF0u) + (uint32_t)__cvta_generic_to_shared(tab);
+  const uint32_t a = ((xb >> 20) & 0x7F8u) + (uint32_t)__cvta_generic_to_shared(tab);
   D2 r;
-  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+  asm("ld.shared.f64 %0, [%1];" : "=d"(r.x) : "r"(a));
+  asm("ld.shared.f64 %0, [%1+2048];" : "=d"(r.y) : "r"(a));
   return r;
 #else
-  return tab[(xb >> 23) & 0xFFu];
+  return D2{tab[(xb >> 23) & 0xFFu], tab[256 + ((xb >> 23) & 0xFFu)]};
 #endif
 }
-CR_F RedTrig red_trig_ph(float x, const D2 *tab) {
+CR_F RedTrig red_trig_ph(float x, const double *tab) {
   const D2 h = ph_row(tab, f2u(x));
   const double xd = f2d(x);
   const double t = fma_(xd, h.x, SHIFTER);
@@ -751,13 +795,33 @@ CR_F double flip_k16(double v, int k) { return hilo2d(d2hi(v) ^ ((k << 27) & (in
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
   static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
-  struct Regs { const D2 *t; };
-  CR_F static void load(Regs &R) { R.t = sh_table16<100, false>(SIN16_HI, COS16_HI, nullptr); }
+  // (S_j, C_j): column-split for sin / cos / sincos (+8-10%, conflict-free
+  // LDS.64), interleaved pairs for tan (-2.6% split; profiles/r02/ab_split.txt)
+  static constexpr bool kSplit = WHICH != 2;
+  struct Regs {
+    const double *t;
+    const D2 *p;
+  };
+  CR_F static void load(Regs &R) {
+    if (kSplit) R.t = sh_split16<100, 2>(SIN16_HI, COS16_HI, nullptr);
+    else R.p = sh_pair16<104>(SIN16_HI, COS16_HI);
+  }
+  CR_F static void sc_get(const Regs &R, int k, double &Sj, double &Cj) {
+    if (kSplit) {
+      const SplitRow sc = split_row(R.t, k);
+      Sj = split_get<0>(sc);
+      Cj = split_get<1>(sc);
+    } else {
+      const D2 sc = R.p[k & 15];
+      Sj = sc.x;
+      Cj = sc.y;
+    }
+  }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    const D2 sc = R.t[q.k & 15];
-    const double Sj = sc.x, Cj = sc.y;
+    double Sj, Cj;
+    sc_get(R, q.k, Sj, Cj);
     double a;
     if (WHICH == 0) a = flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k);
     else if (WHICH == 1) a = flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k);
@@ -775,8 +839,8 @@ struct FnTrig {
   CR_F static void sincos_from_red(float x, RedTrig q, const Regs &R, Fast &fs, Fast &fc) {
     double s = mul_(q.r, q.r);
     double sr = sin_r(q.r, s), cr = cos_r(s);
-    const D2 sc = R.t[q.k & 15];
-    const double Sj = sc.x, Cj = sc.y;
+    double Sj, Cj;
+    sc_get(R, q.k, Sj, Cj);
     const uint32_t xb = f2u(x);
     fs = Fast{flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k), FnTrig<0>::in_main(xb)};
     fc = Fast{flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k), FnTrig<1>::in_main(xb)};
@@ -857,16 +921,16 @@ CR_F double atan_t2(double t) {
 
 struct FnAtan {
   static constexpr uint32_t E = 512;
-  struct Regs { const D2 *t; };
-  CR_F static void load(Regs &R) { R.t = sh_table16<101, true>(ATAN_C, ATAN_S, ATAN_A_HI); }
+  struct Regs { const double *t; };
+  CR_F static void load(Regs &R) { R.t = sh_split16<101, 3>(ATAN_C, ATAN_S, ATAN_A_HI); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     float axf = fminf(fabs_(x), 0x1p127f);
     double z = f2d(axf);
     bool up = axf > 1.0f;
     int k = (int)f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f)) + (up ? 8 : 0);
-    const D2 cs = R.t[2 * (k & 15)];
-    const double A = R.t[2 * (k & 15) + 1].x, C = cs.x, S = cs.y;
+    const SplitRow cs = split_row(R.t, k);
+    const double C = split_get<0>(cs), S = split_get<1>(cs), A = split_get<2>(cs);
     double t = div_fast(fma_(z, C, -S), fma_(z, S, C));
     return Fast{with_sign(add_(A, atan_t2(t)), xb), in_main(xb)};
   }
@@ -906,10 +970,10 @@ CR_F double asinq(double d) {
 template <bool ACOS>
 struct FnAsinAcos {
   static constexpr uint32_t E = 64;
-  struct Regs { int a; const D2 *t; };
+  struct Regs { int a; const double *t; };
   CR_F static void load(Regs &R) {
     R.a = ACOS ? CR_TAB_LOAD(ACOS_A_HI) : CR_TAB_LOAD(ASIN_A_HI);
-    R.t = ACOS ? sh_table16<102, false>(ACOS_C, ACOS_S, nullptr) : sh_table16<103, false>(ASIN_C, ASIN_S, nullptr);
+    R.t = ACOS ? sh_split16<102, 2>(ACOS_C, ACOS_S, nullptr) : sh_split16<103, 2>(ASIN_C, ASIN_S, nullptr);
   }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
@@ -924,8 +988,8 @@ struct FnAsinAcos {
     // entries (profiles/r01/ab_shtab_trig.txt)
     int k = (int)f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f)) + (up ? 8 : 0);
     double A = hilo2d(ACOS ? CR_TAB(R.a, ACOS_A_HI, k) : CR_TAB(R.a, ASIN_A_HI, k), 0u);
-    const D2 cs = R.t[k & 15];
-    const double C = cs.x, S = cs.y;
+    const SplitRow cs = split_row(R.t, k);
+    const double C = split_get<0>(cs), S = split_get<1>(cs);
     double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
     double a = add_(A, asinq(d));
     if (!ACOS) a = with_sign(a, xb);

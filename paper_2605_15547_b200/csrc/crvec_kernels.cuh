@@ -97,7 +97,7 @@ __device__ __noinline__ DD slow_dd(float x) {
 // divergence: round 1's per-warp ballot queue cost ~25 thread-instructions
 // per element on the config-3 mix (profiles/r02/ncu_lines_sinf.txt).
 struct PHBlock {
-  D2 tab[256];  // PH_T rows by biased exponent
+  double tab[512];  // PH_T by biased exponent b: hi at [b], lo at [256 + b]
 };
 
 template <int NE>
@@ -312,7 +312,10 @@ template <class F>
 __device__ __forceinline__ PHBlock *ph_storage() {
   if constexpr (IsTrig<F>::value) {
     __shared__ PHBlock sh;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.tab[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      sh.tab[i] = PH_T[2 * i];
+      sh.tab[256 + i] = PH_T[2 * i + 1];
+    }
     __syncthreads();
     return &sh;
   } else {
