@@ -26,6 +26,61 @@ struct alignas(16) D2 {
 
 
 
+// Column-split shared 16-entry tables: NC columns of 16 doubles (128 bytes
+// each, one column per value). A warp's LDS.64 moves 256 bytes in two
+// 128-byte wavefronts and a column spans each bank exactly once, so any mix
+// of rows is conflict-free; the interleaved 16-byte-pair form (LDS.128)
+// conflicts whenever two lanes of a quarter-warp read rows r and r + 8
+// (ncu: 6.7 wavefronts per LDS.128 instead of 4 in sinf, round 2). Column c
+// of row j: base + 128 c + 8 (j & 15), one address per row and immediate
+// column offsets. W gives a third column as hilo2d(W[i], 0).
+template <int TAG, int NC>
+CR_F const double *sh_split16(const double *A, const double *B, const int *W) {
+#if CR_DEVICE
+  __shared__ __align__(16) double tab[16 * NC];
+#else
+  static double tab[16 * NC];
+#endif
+#if CR_DEVICE
+  if (threadIdx.x < 16) {
+    const int i = threadIdx.x;
+#else
+  for (int i = 0; i < 16; ++i) {
+#endif
+    tab[i] = A[i];
+    if (NC > 1) tab[16 + i] = B[i];
+    if (NC > 2) tab[32 + i] = hilo2d(W[i], 0u);
+  }
+#if CR_DEVICE
+  __syncthreads();
+#endif
+  return tab;
+}
+struct SplitRow {
+#if CR_DEVICE
+  uint32_t a;  // shared address of column 0, row j
+#else
+  const double *p;
+#endif
+};
+CR_F SplitRow split_row(const double *t, int j) {
+#if CR_DEVICE
+  return {(uint32_t)__cvta_generic_to_shared(t) + ((uint32_t)(j & 15) << 3)};
+#else
+  return {t + (j & 15)};
+#endif
+}
+template <int COL>
+CR_F double split_get(SplitRow r) {
+#if CR_DEVICE
+  double v;
+  asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(r.a), "n"(COL * 128));
+  return v;
+#else
+  return r.p[16 * COL];
+#endif
+}
+
 // Polynomials (Horner, coefficients from tools/gen_tables.py).
 CR_F double expq(double r) {
   return fma_(fma_(fma_(fma_(EXPQ[4], r, EXPQ[3]), r, EXPQ[2]), r, EXPQ[1]), r, EXPQ[0]);
@@ -257,30 +312,38 @@ struct HypParts {
 };
 // Fast path uses the rounded table (2^-54 relative per entry): for k = +-1 the
 // difference E+ - E- loses ~5 bits, which the sinh/tanh tolerances cover.
-// Shared table of (2^(j/16), 2^(-j/16 mod 1)) pairs: e^(+a) and e^(-a) come
-// from one LDS.128 (entry k mod 16 holds T[k mod 16] and T[-k mod 16]); 4-5%
-// faster than four SHFL (profiles/r01/ab_shtab_hyp.txt).
+// Shared table of (2^(j/16), 2^(-j/16 mod 1)): e^(+a) and e^(-a) come from
+// row k mod 16 (entry k holds T[k mod 16] and T[-k mod 16]), column-split
+// (two conflict-free LDS.64, see sh_split16; the interleaved LDS.128 form
+// measured 7.4 wavefronts per load in sinhf) - one table read per element
+// was 4-5% faster than four SHFL (profiles/r01/ab_shtab_hyp.txt).
 template <int TAG>
-CR_F const D2 *exp_pm_pairs() {
+CR_F const double *exp_pm_pairs() {
 #if CR_DEVICE
-  __shared__ D2 tab[16];
-  if (threadIdx.x < 16) tab[threadIdx.x] = D2{EXP2J_HI[threadIdx.x], EXP2J_HI[(16 - threadIdx.x) & 15]};
+  __shared__ __align__(16) double tab[32];
+  if (threadIdx.x < 16) {
+    tab[threadIdx.x] = EXP2J_HI[threadIdx.x];
+    tab[16 + threadIdx.x] = EXP2J_HI[(16 - threadIdx.x) & 15];
+  }
   __syncthreads();
   return tab;
 #else
-  static D2 tab[16];
-  for (int i = 0; i < 16; ++i) tab[i] = D2{EXP2J_HI[i], EXP2J_HI[(16 - i) & 15]};
+  static double tab[32];
+  for (int i = 0; i < 16; ++i) {
+    tab[i] = EXP2J_HI[i];
+    tab[16 + i] = EXP2J_HI[(16 - i) & 15];
+  }
   return tab;
 #endif
 }
-using HypTab = const D2 *;
+using HypTab = const double *;
 CR_F HypParts hyp_parts(double ax, HypTab tab) {
   RedExp q = red_exp(ax);
   int kp = q.k, km = -q.k;
   // e^(+-a)/2: the halving folds into the integer exponent add
-  const D2 pm = tab[kp & 15];
-  double Ep = scale2(pm.x, (kp >> 4) - 1);
-  double Em = scale2(pm.y, (km >> 4) - 1);
+  const SplitRow pm = split_row(tab, kp);
+  double Ep = scale2(split_get<0>(pm), (kp >> 4) - 1);
+  double Em = scale2(split_get<1>(pm), (km >> 4) - 1);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(SINHQ[1], s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(COSHQ[1], s, COSHQ[0]), 1.0);
@@ -458,60 +521,6 @@ CR_F const D2 *sh_pair16(const double *A, const double *B) {
   return tab;
 }
 
-// Column-split shared 16-entry tables: NC columns of 16 doubles (128 bytes
-// each, one column per value). A warp's LDS.64 moves 256 bytes in two
-// 128-byte wavefronts and a column spans each bank exactly once, so any mix
-// of rows is conflict-free; the interleaved 16-byte-pair form (LDS.128)
-// conflicts whenever two lanes of a quarter-warp read rows r and r + 8
-// (ncu: 6.7 wavefronts per LDS.128 instead of 4 in sinf, round 2). Column c
-// of row j: base + 128 c + 8 (j & 15), one address per row and immediate
-// column offsets. W gives a third column as hilo2d(W[i], 0).
-template <int TAG, int NC>
-CR_F const double *sh_split16(const double *A, const double *B, const int *W) {
-#if CR_DEVICE
-  __shared__ __align__(16) double tab[16 * NC];
-#else
-  static double tab[16 * NC];
-#endif
-#if CR_DEVICE
-  if (threadIdx.x < 16) {
-    const int i = threadIdx.x;
-#else
-  for (int i = 0; i < 16; ++i) {
-#endif
-    tab[i] = A[i];
-    if (NC > 1) tab[16 + i] = B[i];
-    if (NC > 2) tab[32 + i] = hilo2d(W[i], 0u);
-  }
-#if CR_DEVICE
-  __syncthreads();
-#endif
-  return tab;
-}
-struct SplitRow {
-#if CR_DEVICE
-  uint32_t a;  // shared address of column 0, row j
-#else
-  const double *p;
-#endif
-};
-CR_F SplitRow split_row(const double *t, int j) {
-#if CR_DEVICE
-  return {(uint32_t)__cvta_generic_to_shared(t) + ((uint32_t)(j & 15) << 3)};
-#else
-  return {t + (j & 15)};
-#endif
-}
-template <int COL>
-CR_F double split_get(SplitRow r) {
-#if CR_DEVICE
-  double v;
-  asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(r.a), "n"(COL * 128));
-  return v;
-#else
-  return r.p[16 * COL];
-#endif
-}
 
 
 // x = 2^e * m, m in [0.765625, 1.53125); bin i = 4 bits after the window

@@ -6,6 +6,7 @@ OUT=gpurun_out/final
 mkdir -p $OUT
 nvidia-smi > $OUT/nvsmi.txt 2>&1
 timeout 2400 python -m pytest tests -q -m gpu > $OUT/pytest_gpu.txt 2>&1
+timeout 600 python -c 'import __graft_entry__ as g; g.smoke()' > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/smoke.txt
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 600 python tools/perf.py --reps 20 > $OUT/perf.txt 2>&1
@@ -15,7 +16,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active \
   --clock-control none -k regex:'k_map_vec|k_sincos_vec|k_f64' --csv --log-file $OUT/inst.csv \
   python tools/perf.py --reps 1 > /dev/null 2>&1
-for f in logf log1pf expf sinf asinf; do
+for f in logf log2f log10f log1pf sinf tanf asinf atanf; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_map_vec -s 3 -c 1 \
       -o $OUT/prof_$f python tools/perf.py --fn $f --reps 1 --no-f64 > /dev/null 2>&1
 done
