@@ -724,6 +724,10 @@ CR_F double sin_r(double r, double s) {
   return fma_(mul_(r, s), fma_(fma_(SINQ[2], s, SINQ[1]), s, SINQ[0]), r);
 }
 CR_F double cos_r(double s) { return fma_(s, fma_(fma_(COSQ[2], s, COSQ[1]), s, COSQ[0]), 1.0); }
+// tan r = r + r^3 T(r^2), |r| <= pi/32 (relative error 2^-47.3, tools/gen_tables.py)
+CR_F double tan_r(double r, double s) {
+  return fma_(mul_(r, s), fma_(fma_(fma_(TANQ[3], s, TANQ[2]), s, TANQ[1]), s, TANQ[0]), r);
+}
 // DD sin/cos of r (|r| <= pi/32), Taylor to r^23.
 CR_F void sincos_r_dd(DD r, DD &sr, DD &cr) {
   DD s = dd_mul(r, r);
@@ -828,13 +832,20 @@ struct FnTrig {
   }
   CR_F static Fast from_red(float x, RedTrig q, const Regs &R) {
     double s = mul_(q.r, q.r);
-    double sr = sin_r(q.r, s), cr = cos_r(s);
     double Sj, Cj;
     sc_get(R, q.k, Sj, Cj);
     double a;
-    if (WHICH == 0) a = flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k);
-    else if (WHICH == 1) a = flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k);
-    else a = div_fast(fma_(Sj, cr, mul_(Cj, sr)), fma_(Cj, cr, -mul_(Sj, sr)));
+    if (WHICH == 2) {
+      // tan(a + r) = (S_j + C_j t) / (C_j - S_j t), t = tan r (divided by
+      // cos r > 0; period pi, so no sign flip): 13 FP64 operations + one
+      // MUFU where sin/cos of r and the two products took 17
+      const double t = tan_r(q.r, s);
+      a = div_fast(fma_(Cj, t, Sj), fma_(-Sj, t, Cj));
+    } else {
+      const double sr = sin_r(q.r, s), cr = cos_r(s);
+      if (WHICH == 0) a = flip_k16(fma_(Sj, cr, mul_(Cj, sr)), q.k);
+      else a = flip_k16(fma_(Cj, cr, -mul_(Sj, sr)), q.k);
+    }
     // main: tiny threshold < |x| < inf (sin 2^-12, cos/tan 2^-13)
     return Fast{a, in_main(f2u(x))};
   }

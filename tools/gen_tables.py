@@ -267,6 +267,13 @@ def gen_trig():
     err = rel_err_of(lambda r: 1 + r * r * horner(csd, r * r), mp.cos, -R, R)
     report.append(f"cos poly deg 2 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
     poly_block("COSQ", csd)
+    # tan r = r + r^3 T(r^2), T of degree 3 (tanf's fast path: (S_j + C_j t) / (C_j - S_j t))
+    gt = lambda s: (mp.tan(mp.sqrt(s)) - mp.sqrt(s)) / (mp.sqrt(s) * s) if s > 0 else mp.mpf(1) / 3
+    cs, _ = chebfit(gt, mp.mpf(0), R ** 2, 3)
+    csd = [mp.mpf(d(c)) for c in cs]
+    err = rel_err_of(lambda r: r + r ** 3 * horner(csd, r * r), mp.tan, -R, R)
+    report.append(f"tan poly deg 3 in r^2: max rel err 2^{float(mp.log(err, 2)):.1f}")
+    poly_block("TANQ", csd)
     scalar("INV_PI_16", d(16 / PI))
     h, m, l = split3(PI / 16, 33, 33)
     scalar("PI_16_H", h); scalar("PI_16_M", m); scalar("PI_16_L", l)
