@@ -283,11 +283,13 @@ __device__ __forceinline__ void resolve_rare_staged(const float (&xs)[NE], unsig
     for (int k = 0; k < NE / 4; ++k) row[k] = make_float4(xs[4 * k], xs[4 * k + 1], xs[4 * k + 2], xs[4 * k + 3]);
     const float *rf = reinterpret_cast<const float *>(row);
     float *yl = yf + fbase;  // the lane's first output float: one 64-bit add per step
+    asm("" : "+l"(yl));      // keep it: slot offsets are then 32-bit (one IMAD.WIDE per store)
     int cnt = 0;
     do {
       // highest pending slot first: one FLO (no bit reverse), 32-bit offsets
       const uint32_t e = 31u - (uint32_t)__clz((int)mask);
-      yl[32u * VW * (e / VW) + (e % VW)] = u2f(resolve_one<F, M>(rf[e], cnt));
+      const uint32_t v = resolve_one<F, M>(rf[e], cnt);
+      asm volatile("st.global.b32 [%0], %1;" ::"l"(yl + (32u * VW * (e / VW) + (e % VW))), "r"(v) : "memory");
       mask ^= 1u << e;
     } while (mask);
     if (cnt) atomicAdd(counters, (unsigned long long)cnt);
