@@ -351,6 +351,22 @@ template <> struct RareStore<FnLog1p> { static constexpr bool value = true; };
 template <> struct RareStore<FnSinh> { static constexpr bool value = true; };
 template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = true; };
 
+// L2 bulk prefetch (cp.async.bulk.prefetch.L2, one lane per warp) of the
+// warp's inputs two grid-stride steps ahead: the register double buffer keeps
+// one step (2 KiB per warp) in flight, ~32 KiB per SM at these occupancies,
+// which is short of what HBM latency x bandwidth needs; the L2 copy turns the
+// next-step loads into L2 hits. Measured per function (profiles/r02/
+// ab_prefetch.txt): exp/exp2/exp10, the log family and cosh +1.5..3.5% per
+// launch; issue-bound kernels (trig, inverse trig, sinh, tanh) lose 2-5% and
+// expm1 / rsqrt ~1%, so they go without it.
+template <class F> struct PrefetchL2 { static constexpr bool value = false; };
+template <> struct PrefetchL2<FnExp> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnExp2> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnExp10> { static constexpr bool value = true; };
+template <int B> struct PrefetchL2<FnLogB<B>> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnLog1p> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnCosh> { static constexpr bool value = true; };
+
 template <class F>
 struct KernelShape {
   static constexpr int vw = 4, nv = 2, minb = 3;
@@ -381,6 +397,13 @@ __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> 
                                          const typename F::Regs &R, PHBlock *sh,
                                          unsigned long long *counters) {
   float xs[VW * NV];
+  if constexpr (PrefetchL2<F>::value) {  // the warp's inputs two steps ahead into L2: one bulk prefetch
+    const uint32_t wb = base - (threadIdx.x & 31) + 2u * stride;
+    if ((threadIdx.x & 31) == 0 && wb + 32u * NV <= nv)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + wb),
+                   "r"((uint32_t)(32 * NV * sizeof(Vec<VW>)))
+                   : "memory");
+  }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t in = base + stride + 32 * k;
