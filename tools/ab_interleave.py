@@ -29,6 +29,8 @@ def load(v):
     L = ctypes.CDLL(p)
     L.crvec_eval_f32_dev.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    for f in ("crvec_exp2_dev", "crvec_log_dev"):
+        getattr(L, f).argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
     return L
 
 
@@ -45,7 +47,35 @@ def main():
     libs = [load(v) for v in a.variants]
     s = torch.cuda.current_stream()
     sp = ctypes.c_void_p(s.cuda_stream)
+    print(f"-- variants: {a.variants}")
     names = a.fn or (crvec.F32_FUNCS + ["sincosf"])
+    if "f64" in names:  # binary64 pair: 2^26 uniform inputs as in tools/perf.py
+        names = [m for m in names if m != "f64"]
+        n64 = 1 << 26
+        rng = np.random.default_rng(5)
+        for nm, xs in (("exp2", rng.uniform(-20, 20, n64)), ("log", rng.uniform(0.125, 8, n64))):
+            x = torch.from_numpy(xs).cuda()
+            yy = torch.empty_like(x)
+            fns = [getattr(L, f"crvec_{nm}_dev") for L in libs]
+            for fn in fns:
+                for _ in range(2):
+                    fn(x.data_ptr(), yy.data_ptr(), n64, a.mode, sp)
+            torch.cuda.synchronize()
+            per = [[] for _ in libs]
+            for _ in range(a.rounds):
+                for i, fn in enumerate(fns):
+                    ts = []
+                    for _ in range(a.reps):
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(s)
+                        fn(x.data_ptr(), yy.data_ptr(), n64, a.mode, sp)
+                        e1.record(s)
+                        torch.cuda.synchronize()
+                        ts.append(e0.elapsed_time(e1))
+                    per[i].append(float(np.median(ts)))
+            g = [n64 / (float(np.median(p)) * 1e-3) / 1e9 for p in per]
+            print(f"{nm + '(f64)':8s} " + " ".join(f"{v:9.1f}" for v in g) + "   " +
+                  " ".join(f"{v / g[0]:7.3f}" for v in g[1:]), flush=True)
     y = torch.empty(n, dtype=torch.float32, device="cuda")
     y2 = torch.empty(n, dtype=torch.float32, device="cuda")
     print(f"-- {a.dist}, 2^28, mode {a.mode}: Gelem/s (median of {a.rounds} interleaved rounds x "
