@@ -477,9 +477,11 @@ template <int TAG>
 CR_F const D2 *log_pairs(const double *L) {
 #if CR_DEVICE
   __shared__ __align__(256) D2 tab[16];  // 256-aligned: see log_pair()
-  // The user shared window starts after a reserved region, so the alignment
-  // of the shared *address* is checked, not assumed (a misplaced table would
-  // otherwise read wrong rows silently).
+  // The OR-ed row offset needs the shared *address* 256-aligned. User shared
+  // memory starts 1 KiB into the CTA's window (sm_100 reserves the first
+  // 1 KiB), so declared alignments up to 1 KiB hold for absolute addresses
+  // (a 4 KiB alignment did not: an OR-addressed Payne-Hanek table read wrong
+  // rows in a round-2 build). The check costs one test per thread.
   if (((uint32_t)__cvta_generic_to_shared(tab) & 255u) != 0u) __trap();
   if (threadIdx.x < 16) tab[threadIdx.x] = D2{hilo2d(LOG_C_HI[threadIdx.x], 0u), L[threadIdx.x]};
   __syncthreads();
