@@ -436,11 +436,21 @@ struct FnTanh {
   CR_F static void load(Regs &R) { R.t = exp_tab<125>(); }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
-    RedExp q = red_exp(mul_(2.0, f2d(fminf(fabs_(x), 10.0f))));
-    int e = q.k >> 4;
-    double T = scale2(exp_t(R.t, q.k), e);
-    double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
-    double em1 = fma_(T, p, sub_(T, 1.0));
+    // reduction of 2|x| with the x2 folded in: k = RN(2|x| 16/ln2), h = r/2 =
+    // |x| - k ln2/32 (Cody-Waite on the halved constants, exact first step),
+    // (e^r - 1)/2 = h + h^2 2Q(2h); E = T e^r - 1 = 2T (e^r - 1)/2 + (T - 1)
+    const double xd = f2d(fminf(fabs_(x), 10.0f));
+    const double t = fma_(xd, INV_LN2_32, SHIFTER);
+    const double kd = sub_(t, SHIFTER);
+    double h = fma_(kd, -LN2_32_H, xd);  // exact
+    h = fma_(kd, -LN2_32_M, h);
+    const int k = (int)d2lo(t), e = k >> 4;
+    const double Tj = exp_t(R.t, k);
+    const double T = scale2(Tj, e), T2 = scale2(Tj, e + 1);
+    const double q = fma_(fma_(fma_(fma_(EXPQ_HALF[4], h, EXPQ_HALF[3]), h, EXPQ_HALF[2]), h, EXPQ_HALF[1]), h,
+                          EXPQ_HALF[0]);
+    const double ph = fma_(mul_(h, h), q, h);
+    double em1 = fma_(T2, ph, sub_(T, 1.0));
     return Fast{with_sign(div_fast(em1, add_(em1, 2.0)), xb), in_main(xb)};
   }
   // main: 2^-12 < |x| < inf. |x| > 10 takes the clamp: tanh(10) lies in

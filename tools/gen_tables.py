@@ -128,9 +128,14 @@ def gen_exp():
         err = rel_err_of(lambda r: r + r * r * horner(csd, r), mp.expm1, -R_EXP, R_EXP)
         report.append(f"expm1 poly r+r^2*Q deg(Q)={deg}: max rel err 2^{float(mp.log(err, 2)):.1f}")
         poly_block(name, csd)
+    # tanhf works on h = r/2 (the x2 of expm1(2|x|) folded into the reduction):
+    # (e^(2h) - 1)/2 = h + h^2 * 2 Q(2h), coefficients EXPQ[i] * 2^(i+1) (exact)
+    poly_block("EXPQ_HALF", [c * mp.mpf(2) ** (i + 1) for i, c in enumerate(csd)])
     h, m, l = split3(LN2 / 16, 40, 40)
     scalar("LN2_16_H", h); scalar("LN2_16_M", m); scalar("LN2_16_L", l)
+    scalar("LN2_32_H", h / 2); scalar("LN2_32_M", m / 2)  # exact halves
     scalar("INV_LN2_16", d(16 / LN2))
+    scalar("INV_LN2_32", d(32 / LN2))
     scalar("LN2_D", d(LN2))
     scalar("LN2_DL", d(LN2 - d(LN2)))
     LOG2_10 = mp.log(10, 2)
