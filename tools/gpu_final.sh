@@ -19,7 +19,7 @@ timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,launch_
 # full captures go to /tmp (gpurun copies back <= 64 MiB); only the raw CSV
 # pages and the per-line census come back
 REPS=/tmp/final_reps; mkdir -p $REPS
-for f in logf log2f log10f log1pf sinf tanf asinf atanf; do
+for f in logf log2f log10f log1pf sinf cosf tanf asinf acosf atanf sinhf tanhf; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_map_vec -s 3 -c 1 \
       -o $REPS/prof_$f python tools/perf.py --fn $f --reps 1 --no-f64 > /dev/null 2>&1
   ncu -i $REPS/prof_$f.ncu-rep --page raw --csv > $OUT/ncu_full_$f.csv 2>/dev/null
