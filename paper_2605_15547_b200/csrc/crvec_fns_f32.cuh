@@ -548,7 +548,15 @@ CR_F RedLog red_log(double xd) {
   int h = d2hi(xd);
   int hh = h - 0x3FE88000;
   int e = hh >> 20;
-  return {e, hh >> 16, hh, hilo2d(h - (int)((uint32_t)e << 20), d2lo(xd))};
+#if CR_DEVICE
+  // m's high word h - e 2^20 as one IMAD (the shift-and-subtract form compiles
+  // to LOP3 + IADD on the ALU pipe)
+  int mh;
+  asm("mad.lo.s32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(e), "r"(h));
+#else
+  int mh = h - (int)((uint32_t)e << 20);
+#endif
+  return {e, hh >> 16, hh, hilo2d(mh, d2lo(xd))};
 }
 
 template <int BASE>  // 0: ln, 2: log2, 10: log10
