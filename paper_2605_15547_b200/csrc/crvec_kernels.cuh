@@ -392,16 +392,20 @@ template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 8, nv
 // buffers swapped, so the double buffer needs no register moves.
 template <class F, int M, int VW, int NV>
 __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> *__restrict__ y,
-                                         uint32_t nv, uint32_t base, uint32_t stride,
+                                         uint32_t nv, uint32_t base, uint32_t ub, uint32_t stride,
                                          const Vec<VW> (&cur)[NV], Vec<VW> (&nxt)[NV],
                                          const typename F::Regs &R, PHBlock *sh,
                                          unsigned long long *counters) {
   float xs[VW * NV];
-  if constexpr (PrefetchL2<F>::value) {  // the warp's inputs two steps ahead into L2: one bulk prefetch
-    const uint32_t wb = base - (threadIdx.x & 31) + 2u * stride;
-    if ((threadIdx.x & 31) == 0 && wb + 32u * NV <= nv)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + wb),
-                   "r"((uint32_t)(32 * NV * sizeof(Vec<VW>)))
+  if constexpr (PrefetchL2<F>::value) {
+    // the block's inputs two steps ahead into L2: one bulk prefetch by thread 0,
+    // from the block base ub (uniform: blockIdx, stride), so the operands sit
+    // in uniform registers (a per-warp address derived from threadIdx made
+    // ptxas wrap the instruction in a waterfall loop, ~10 instructions)
+    const uint32_t pb = ub + 2u * stride;
+    if (threadIdx.x == 0 && pb + (uint32_t)(kThreads * NV) <= nv)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + pb),
+                   "r"((uint32_t)(kThreads * NV * sizeof(Vec<VW>)))
                    : "memory");
   }
 #pragma unroll
@@ -427,7 +431,11 @@ __device__ __forceinline__ void map_step(const Vec<VW> *__restrict__ x, Vec<VW> 
         resolve_rare_store<F, M, VW * NV, VW>(xs, mask, (float *)y, (uint64_t)VW * base, counters);
     }
   } else {
-    eval_lanes<F, M, VW * NV>(xs, ys, R, sh, counters);
+    unsigned mask = fast_eval<F, M, VW * NV>(xs, ys, R, sh);
+#pragma unroll
+    for (int k = 0; k < NV; ++k)  // stale inputs past the end
+      if (base + 32 * k >= nv) mask &= ~(((1u << VW) - 1u) << (VW * k));
+    if (__any_sync(kFull, mask != 0)) resolve_rare<F, M, VW * NV>(xs, ys, mask, counters);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const uint32_t i = base + 32 * k;
@@ -461,12 +469,18 @@ __global__ void __launch_bounds__(kThreads, KernelShape<F>::minb)
     vb[k] = va[k];
     if (base + 32 * k < nv) va[k] = ld_vec<VW>(x + base + 32 * k);
   }
-  while (base - lane < nv) {
-    map_step<F, M, VW, NV>(x, y, nv, base, stride, va, vb, R, sh, counters);
-    base += stride;
-    if (base - lane >= nv) break;
-    map_step<F, M, VW, NV>(x, y, nv, base, stride, vb, va, R, sh, counters);
-    base += stride;
+  // block-uniform loop over ub, the block's first vector of the step (kept in
+  // uniform registers: the L2 prefetch's operands need no waterfall loop); a
+  // warp whose part of the last step lies past nv skips it (warp-uniform test)
+  // block-uniform loop over ub, the block's first vector of the step (kept in
+  // uniform registers: the L2 prefetch's operands need no waterfall loop); a
+  // warp whose part of the last step lies past nv runs it with every load,
+  // store and rare slot masked off
+  const uint32_t wofs = base - blockIdx.x * (uint32_t)(kThreads * NV);  // warp offset + lane
+  for (uint32_t ub = blockIdx.x * (uint32_t)(kThreads * NV); ub < nv; ub += 2u * stride) {
+    map_step<F, M, VW, NV>(x, y, nv, ub + wofs, ub, stride, va, vb, R, sh, counters);
+    if (ub + stride >= nv) break;
+    map_step<F, M, VW, NV>(x, y, nv, ub + stride + wofs, ub + stride, stride, vb, va, R, sh, counters);
   }
 }
 
