@@ -356,13 +356,14 @@ template <int W> struct RareStore<FnTrig<W>> { static constexpr bool value = tru
 // one step (2 KiB per warp) in flight, ~32 KiB per SM at these occupancies,
 // which is short of what HBM latency x bandwidth needs; the L2 copy turns the
 // next-step loads into L2 hits. Measured per function (profiles/r02/
-// ab_prefetch.txt): exp/exp2/exp10, the log family and cosh +1.5..3.5% per
-// launch; issue-bound kernels (trig, inverse trig, sinh, tanh) lose 2-5% and
-// expm1 / rsqrt ~1%, so they go without it.
+// ab_prefetch.txt): exp/exp2/exp10/expm1, the log family and cosh
+// +1.5..3.5% per launch; issue-bound kernels (trig, inverse trig, sinh, tanh)
+// and rsqrt lose 1-4%, so they go without it.
 template <class F> struct PrefetchL2 { static constexpr bool value = false; };
 template <> struct PrefetchL2<FnExp> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnExp2> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnExp10> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnExpm1> { static constexpr bool value = true; };
 template <int B> struct PrefetchL2<FnLogB<B>> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnLog1p> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnCosh> { static constexpr bool value = true; };
