@@ -430,9 +430,16 @@ struct LogdV {
 CR_F LogdV logd_value(double xs, int eadj, const F64Tab &T) {
   int h = d2hi(xs);
   int hh = h - 0x3FE80000;
-  int e = (hh >> 20) + eadj;
+  const int e0 = hh >> 20;
+  int e = e0 + eadj;
   int i = (hh >> 11) & 511;
-  double m = hilo2d(h - ((hh >> 20) << 20), d2lo(xs));
+#if CR_DEVICE
+  int mh;  // h - e0 2^20 as one IMAD (the shift-and-subtract form is LOP3 + IADD)
+  asm("mad.lo.s32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(e0), "r"(h));
+#else
+  int mh = h - (int)((uint32_t)e0 << 20);
+#endif
+  double m = hilo2d(mh, d2lo(xs));
   const Pair64 cl = T.lc[i];
   double r = fma_(m, cl.a, -1.0);                  // exact
   DD s = two_prod(r, r);                          // r^2 exact
