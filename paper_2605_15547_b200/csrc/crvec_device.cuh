@@ -280,6 +280,20 @@ CR_F double sqrt_fast(double a) {
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);
 // valid while the result stays normal.
 CR_F double scale2(double a, int e) { return hilo2d(d2hi(a) + (e << 20), d2lo(a)); }
+// The same with the exponent add forced into one IMAD (the shift-and-add
+// form compiles to 2-3 ALU ops). Used where it is measured and verified
+// (exp family, expm1, tanh); in the sinh/cosh assembly (two scaled reads of
+// one shared row) this form produced wrong results in a round-2 build and
+// is not used there.
+CR_F double scale2_imad(double a, int e) {
+#if CR_DEVICE
+  int h;
+  asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(h) : "r"(e), "r"(d2hi(a)));
+  return hilo2d(h, d2lo(a));
+#else
+  return scale2(a, e);
+#endif
+}
 
 // Division num/den to ~2^-52 relative: MUFU seed, one Newton step, one
 // residual correction (6 FP64 ops). The residual step is required: a product

@@ -120,7 +120,7 @@ template <class Tab>
 CR_F double exp_core(int k, double r, Tab tab) {
   double T = exp_t(tab, k);
   double p = fma_(mul_(r, r), expq(r), r);  // e^r - 1
-  return scale2(fma_(T, p, T), k >> 4);
+  return scale2_imad(fma_(T, p, T), k >> 4);
 }
 
 // Cubic-Q variant (2^-40.1 relative on e^r - 1, i.e. < 2^-45.5 on the
@@ -130,7 +130,7 @@ template <class Tab>
 CR_F double exp_core3(int k, double r, Tab tab) {
   double T = exp_t(tab, k);
   double p = fma_(mul_(r, r), expq3(r), r);  // e^r - 1
-  return scale2(fma_(T, p, T), k >> 4);
+  return scale2_imad(fma_(T, p, T), k >> 4);
 }
 // Non-main lanes of exp / exp2 / exp10: NaN, +-0 -> 1, +Inf -> +Inf,
 // -Inf -> +0, tiny |x|: b^x lies in the gap beside 1 (above for x > 0).
@@ -273,7 +273,7 @@ struct FnExpm1 {
     uint32_t xb = f2u(x);
     RedExp q = red_exp(f2d(fminf(fmaxf(x, -18.5f), 89.5f)));
     int e = q.k >> 4;
-    double T = scale2(exp_t(R.t, q.k), e);
+    double T = scale2_imad(exp_t(R.t, q.k), e);
     double p = fma_(mul_(q.r, q.r), expq(q.r), q.r);
     // main: 2^-26 < |x| < inf and x >= -18
     return Fast{fma_(T, p, sub_(T, 1.0)), in_main(xb)};
@@ -446,7 +446,7 @@ struct FnTanh {
     h = fma_(kd, -LN2_32_M, h);
     const int k = (int)d2lo(t), e = k >> 4;
     const double Tj = exp_t(R.t, k);
-    const double T = scale2(Tj, e), T2 = scale2(Tj, e + 1);
+    const double T = scale2_imad(Tj, e), T2 = scale2_imad(Tj, e + 1);
     const double q = fma_(fma_(fma_(fma_(EXPQ_HALF[4], h, EXPQ_HALF[3]), h, EXPQ_HALF[2]), h, EXPQ_HALF[1]), h,
                           EXPQ_HALF[0]);
     const double ph = fma_(mul_(h, h), q, h);

@@ -393,7 +393,7 @@ CR_F F64Out exp2d_fast(double x, const F64Tab &T) {
   F64Out r = round_test64<M>(e.V.hi, e.V.lo, EPS_EXP2D * dabs(e.V.hi));
   if (x < -1022.0) r.decided = false;  // subnormal result: accurate path
   // y in [1, 2]: the exponent add is exact, 2 * 2^1023 correctly gives +Inf
-  r.y = hilo2d(d2hi(r.y) + (e.N << 20), d2lo(r.y));
+  r.y = scale2(r.y, e.N);
   return r;
 }
 
@@ -407,7 +407,7 @@ CR_F F64Out exp2d_main_path(double x, const F64Tab &T) {
   const Exp2dV e = exp2d_value(ok ? x : 0.5, T);
   F64Out r = round_test64<M>(e.V.hi, e.V.lo, EPS_EXP2D * dabs(e.V.hi));
   r.decided = r.decided && ok && !(e.R == 0.0 && (e.k & 4095) == 0);
-  r.y = hilo2d(d2hi(r.y) + (e.N << 20), d2lo(r.y));
+  r.y = scale2(r.y, e.N);
   return r;
 }
 
