@@ -281,10 +281,11 @@ CR_F double sqrt_fast(double a) {
 // valid while the result stays normal.
 CR_F double scale2(double a, int e) { return hilo2d(d2hi(a) + (e << 20), d2lo(a)); }
 // The same with the exponent add forced into one IMAD (the shift-and-add
-// form compiles to 2-3 ALU ops). Used where it is measured and verified
-// (exp family, expm1, tanh); in the sinh/cosh assembly (two scaled reads of
-// one shared row) this form produced wrong results in a round-2 build and
-// is not used there.
+// form compiles to 2-3 ALU ops). Do not feed it e = (-k) >> n: ptxas 12.9
+// folds the negated shift into a LEA.HI.SX32 with a negated operand that
+// computes -(k >> n) instead (found by the exhaustive sinh/cosh sweep,
+// reproduced standalone); hyp_parts passes -(k + 15) >> 4 to
+// scale2_imad_neg instead.
 CR_F double scale2_imad(double a, int e) {
 #if CR_DEVICE
   int h;
@@ -292,6 +293,16 @@ CR_F double scale2_imad(double a, int e) {
   return hilo2d(h, d2lo(a));
 #else
   return scale2(a, e);
+#endif
+}
+// a * 2^-u (hi - u 2^20 as one IMAD)
+CR_F double scale2_imad_neg(double a, int u) {
+#if CR_DEVICE
+  int h;
+  asm("mad.lo.s32 %0, %1, -1048576, %2;" : "=r"(h) : "r"(u), "r"(d2hi(a)));
+  return hilo2d(h, d2lo(a));
+#else
+  return scale2(a, -u);
 #endif
 }
 

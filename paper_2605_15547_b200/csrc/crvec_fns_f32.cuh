@@ -322,16 +322,16 @@ CR_F const double *exp_pm_pairs() {
 #if CR_DEVICE
   __shared__ __align__(16) double tab[32];
   if (threadIdx.x < 16) {
-    tab[threadIdx.x] = EXP2J_HI[threadIdx.x];
-    tab[16 + threadIdx.x] = EXP2J_HI[(16 - threadIdx.x) & 15];
+    tab[threadIdx.x] = 0.5 * EXP2J_HI[threadIdx.x];  // halved: e^(+-a)/2 (exact)
+    tab[16 + threadIdx.x] = 0.5 * EXP2J_HI[(16 - threadIdx.x) & 15];
   }
   __syncthreads();
   return tab;
 #else
   static double tab[32];
   for (int i = 0; i < 16; ++i) {
-    tab[i] = EXP2J_HI[i];
-    tab[16 + i] = EXP2J_HI[(16 - i) & 15];
+    tab[i] = 0.5 * EXP2J_HI[i];
+    tab[16 + i] = 0.5 * EXP2J_HI[(16 - i) & 15];
   }
   return tab;
 #endif
@@ -339,11 +339,12 @@ CR_F const double *exp_pm_pairs() {
 using HypTab = const double *;
 CR_F HypParts hyp_parts(double ax, HypTab tab) {
   RedExp q = red_exp(ax);
-  int kp = q.k, km = -q.k;
-  // e^(+-a)/2: the halving folds into the integer exponent add
+  const int kp = q.k;
+  // e^(+-a)/2 from the halved table: 2^(k>>4) and 2^((-k)>>4) = 2^-((k+15)>>4)
+  // as one IMAD each on the exponent field
   const SplitRow pm = split_row(tab, kp);
-  double Ep = scale2(split_get<0>(pm), (kp >> 4) - 1);
-  double Em = scale2(split_get<1>(pm), (km >> 4) - 1);
+  double Ep = scale2_imad(split_get<0>(pm), kp >> 4);
+  double Em = scale2_imad_neg(split_get<1>(pm), (kp + 15) >> 4);
   double s = mul_(q.r, q.r);
   double sr = fma_(mul_(q.r, s), fma_(SINHQ[1], s, SINHQ[0]), q.r);
   double cr = fma_(s, fma_(COSHQ[1], s, COSHQ[0]), 1.0);
