@@ -1011,10 +1011,11 @@ CR_F double asinq(double d) {
 template <bool ACOS>
 struct FnAsinAcos {
   static constexpr uint32_t E = 64;
-  struct Regs { int a; const double *t; };
+  struct Regs { const double *t; };
   CR_F static void load(Regs &R) {
-    R.a = ACOS ? CR_TAB_LOAD(ACOS_A_HI) : CR_TAB_LOAD(ASIN_A_HI);
-    R.t = ACOS ? sh_split16<102, 2>(ACOS_C, ACOS_S, nullptr) : sh_split16<103, 2>(ASIN_C, ASIN_S, nullptr);
+    // (cos, sin, angle) columns: the angle is a third conflict-free LDS.64 off
+    // the same row address (one SHFL + a zero-word move before)
+    R.t = ACOS ? sh_split16<102, 3>(ACOS_C, ACOS_S, ACOS_A_HI) : sh_split16<103, 3>(ASIN_C, ASIN_S, ASIN_A_HI);
   }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
@@ -1023,14 +1024,12 @@ struct FnAsinAcos {
     double s = sqrt_fast(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
     float sf = (float)s;
     bool up = axf > sf;
-    // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; the
-    // angle is a register table (one SHFL, lane k mod 32), (cos, sin) a
-    // shared pair (one LDS.128): +6% over five SHFL, and over 32-byte shared
-    // entries (profiles/r01/ab_shtab_trig.txt)
+    // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; (cos,
+    // sin, angle) from three columns of one shared row (round 2; round 1 had
+    // the angle in a register table, profiles/r01/ab_shtab_trig.txt)
     int k = (int)f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f)) + (up ? 8 : 0);
-    double A = hilo2d(ACOS ? CR_TAB(R.a, ACOS_A_HI, k) : CR_TAB(R.a, ASIN_A_HI, k), 0u);
     const SplitRow cs = split_row(R.t, k);
-    const double C = split_get<0>(cs), S = split_get<1>(cs);
+    const double C = split_get<0>(cs), S = split_get<1>(cs), A = split_get<2>(cs);
     double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
     double a = add_(A, asinq(d));
     if (!ACOS) a = with_sign(a, xb);
