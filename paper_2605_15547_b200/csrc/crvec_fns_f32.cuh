@@ -458,6 +458,9 @@ struct FnTanh {
   // (1 - 2^-27, 1), which holds no binary32 rounding boundary, so it rounds
   // like the true value in every mode.
   CR_F static bool in_main(uint32_t xb) { return in_range(xb << 1, 0x73000002u, 0xFF000000u); }
+  // map kernels: main <=> 2^-12 < |x| <= FLT_MAX (float compares, same set as in_main)
+  static constexpr bool kMainAbs = true;
+  static constexpr float kMainLo = 0x1p-12f, kMainHi = 0x1.fffffep127f;
   template <int M>
   CR_F static uint32_t special(float x) {
     uint32_t xb = f2u(x), az = xb << 1;
