@@ -1,4 +1,4 @@
-// trig family kernels: sinf, cosf, tanf, sincosf (warp-cooperative Payne-Hanek).
+// trig family kernels: sinf, cosf, tanf, sincosf (warp-uniform Payne-Hanek).
 #include "crvec_kernels.cuh"
 namespace crvec {
 void register_trig(FnEntry *t) {

@@ -1,6 +1,6 @@
-// Kernel templates: streaming map kernels (128-bit coalesced I/O, grid-stride,
-// warp-uniform loops so register tables can use __shfl_sync), the
-// warp-cooperative Payne-Hanek path, the rare accurate-path fallback, and the
+// Kernel templates: streaming map kernels (128/256-bit coalesced I/O, block-
+// uniform grid-stride loops so register tables can use __shfl_sync), the
+// warp-uniform Payne-Hanek reduction, the rare accurate-path fallback, and the
 // exhaustive-sweep kernel with a commutative per-chunk hash.
 #pragma once
 #include <cuda_runtime.h>
