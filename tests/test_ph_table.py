@@ -1,4 +1,5 @@
-"""CPU checks of the trig fast path's exponent-indexed Payne-Hanek table
+"""CPU checks of round-2 fast-path constants: the tanhf halved reduction, the
+tanf polynomial, and the trig fast path's exponent-indexed Payne-Hanek table
 (PH_T in csrc/crvec_tables.inc, tools/gen_tables.py gen_ph_table) and of the
 reduction it feeds (red_trig_ph in csrc/crvec_fns_f32.cuh), restated in exact
 rational arithmetic:
@@ -83,3 +84,42 @@ def test_rows_cover_every_exponent(table):
     # row 255 (Inf / NaN) is never used on the main path; every other row is set
     assert table[2 * 255] == 0.0 and table[2 * 255 + 1] == 0.0
     assert all(table[2 * b] != 0.0 or table[2 * b + 1] != 0.0 for b in range(255))
+
+
+def _arr(name):
+    txt = open(INC).read()
+    m = re.search(name + r"\[(\d+)\] = \{(.*?)\};", txt, flags=re.S)
+    return [float.fromhex(v.strip()) if "0x" in v else float(v) for v in m.group(2).split(",") if v.strip()]
+
+
+def _scalar(name):
+    m = re.search(r"CR_CONST double " + name + r" = ([^;]+);", open(INC).read())
+    v = m.group(1).strip()
+    return float.fromhex(v) if "0x" in v else float(v)
+
+
+def test_tanh_halved_constants_are_exact_scalings():
+    """tanhf works on h = r/2 (FnTanh::fast): its coefficients and Cody-Waite
+    constants must be exact power-of-two scalings of the exp family's."""
+    q, qh = _arr("EXPQ"), _arr("EXPQ_HALF")
+    assert len(q) == len(qh) == 5
+    for i, (a, b) in enumerate(zip(q, qh)):
+        assert Fraction(b) == Fraction(a) * 2 ** (i + 1)
+    assert Fraction(_scalar("LN2_32_H")) * 2 == Fraction(_scalar("LN2_16_H"))
+    assert Fraction(_scalar("LN2_32_M")) * 2 == Fraction(_scalar("LN2_16_M"))
+    assert _scalar("INV_LN2_32") == 2 * _scalar("INV_LN2_16")
+
+
+def test_tan_polynomial_accuracy():
+    """t = r + r^3 T(r^2) on |r| <= pi/32 (1 + 5e-4): relative error < 2^-47
+    (tanf's budget is E = 1024 double ulps, 2^-43)."""
+    T = [Fraction(v) for v in _arr("TANQ")]
+    with mp.workprec(200):
+        R = mp.pi / 32 * mp.mpf("1.0005")
+        worst = mp.mpf(0)
+        for i in range(1, 801):
+            r = R * i / 800
+            s = r * r
+            p = sum(mp.mpf(c.numerator) / c.denominator * s ** k for k, c in enumerate(T))
+            worst = max(worst, abs((r + r * s * p) / mp.tan(r) - 1))
+        assert worst < mp.mpf(2) ** -47
