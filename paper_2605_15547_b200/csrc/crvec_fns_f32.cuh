@@ -70,6 +70,17 @@ CR_F SplitRow split_row(const double *t, int j) {
   return {t + (j & 15)};
 #endif
 }
+// Row j + 8 up of a sh_split16 table, j in [0, 7] left by the shifter trick
+// in the low bits of kb = bits of (float)(j + 1.5 2^23): the shifter bias and
+// the +8 rows ride in one select-constant of an IMAD (kb 8 + c), no masking.
+CR_F SplitRow split_row_kb(const double *t, uint32_t kb, bool up) {
+#if CR_DEVICE
+  const uint32_t c = (up ? 64u : 0u) - (0x4B400000u << 3);
+  return {(uint32_t)__cvta_generic_to_shared(t) + (kb * 8u + c)};
+#else
+  return {t + ((kb & 7u) + (up ? 8u : 0u))};
+#endif
+}
 template <int COL>
 CR_F double split_get(SplitRow r) {
 #if CR_DEVICE
@@ -972,8 +983,8 @@ struct FnAtan {
     float axf = fminf(fabs_(x), 0x1p127f);
     double z = f2d(axf);
     bool up = axf > 1.0f;
-    int k = (int)f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f)) + (up ? 8 : 0);
-    const SplitRow cs = split_row(R.t, k);
+    const uint32_t kb = f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f));  // j <= 7
+    const SplitRow cs = split_row_kb(R.t, kb, up);
     const double C = split_get<0>(cs), S = split_get<1>(cs), A = split_get<2>(cs);
     double t = div_fast(fma_(z, C, -S), fma_(z, S, C));
     return Fast{with_sign(add_(A, atan_t2(t)), xb), in_main(xb)};
@@ -1030,8 +1041,8 @@ struct FnAsinAcos {
     // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; (cos,
     // sin, angle) from three columns of one shared row (round 2; round 1 had
     // the angle in a register table, profiles/r01/ab_shtab_trig.txt)
-    int k = (int)f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f)) + (up ? 8 : 0);
-    const SplitRow cs = split_row(R.t, k);
+    const uint32_t kb = f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f));  // j <= 7
+    const SplitRow cs = split_row_kb(R.t, kb, up);
     const double C = split_get<0>(cs), S = split_get<1>(cs), A = split_get<2>(cs);
     double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
     double a = add_(A, asinq(d));
