@@ -89,10 +89,12 @@ def test_kernels_compiled_for_sm100a():
     s = sass("_ZN5crvec9k_map_vecINS_6FnLogBILi0EEELi0EEEvPKfPfjPy")
     for op in ("DFMA", "LDS.128", "LDG.E.NA", "STG.E.EF", "F2F.F32.F64"):
         assert op in s, op
-    # asinf: angle from a register table read with __shfl_sync
+    # asinf: (C, S, angle) from the column-split shared table (round 2: the
+    # angle moved from a __shfl_sync register table to a third column)
     s = sass("_ZN5crvec9k_map_vecINS_10FnAsinAcosILb0EEELi0EEEvPKfPfjPy")
-    for op in ("DFMA", "SHFL.IDX", "LDG.E", "STG.E", "F2F.F32.F64"):
+    for op in ("DFMA", "LDS.64", "LDG.E", "STG.E", "F2F.F32.F64"):
         assert op in s, op
+    assert "SHFL.IDX" not in s
 
 
 def test_cpp_compat_header_compiles(lib, tmp_path):
