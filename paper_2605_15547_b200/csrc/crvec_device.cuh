@@ -111,8 +111,12 @@ CR_F double add_M(double a, double b) {
 CR_F double f2d(float f) { return (double)f; }
 CR_F double dabs(double a) { return std::fabs(a); }
 CR_F float fabs_(float a) { return std::fabs(a); }
-CR_F double rcp_approx(double x) { return (double)(float)(1.0 / x); }  // optimistic: MUFU.RCP64H is coarser
-CR_F double rsqrt_approx(double x) { return (double)(float)(1.0 / std::sqrt(x)); }
+// MUFU.RCP64H / RSQ64H seeds modelled pessimistically: the exact value cut
+// to 19 fraction bits (relative error < 2^-19; measured on B200: 2^-19.9 /
+// 2^-19.0 for |1 - x r| / |1 - x y^2|, tools/mufu_probe.cu)
+CR_F double seed19(double v) { uint64_t u; std::memcpy(&u, &v, 8); u &= ~((1ull << 33) - 1); std::memcpy(&v, &u, 8); return v; }
+CR_F double rcp_approx(double x) { return seed19(1.0 / x); }
+CR_F double rsqrt_approx(double x) { return seed19(1.0 / std::sqrt(x)); }
 CR_F float rcp_approx_f(float x) { return 1.0f / x; }
 CR_F double sqrt_rn(double x) { return std::sqrt(x); }
 CR_F int clz32(uint32_t v) { return v ? __builtin_clz(v) : 32; }
@@ -265,16 +269,16 @@ CR_F bool nan_bits(uint32_t xb) { return (xb << 1) > 0xFF000000u; }
 CR_F uint32_t quiet_bits(uint32_t xb) { return xb | 0x00400000u; }
 
 // sqrt(a) for a normal, positive a to ~2^-52 relative (a = 0 gives NaN: the
-// callers keep such lanes off the main path): MUFU.RSQ64H seed y0, one
-// coupled Newton step on (s, h) = (a*y0, y0/2), one Karp-Markstein
-// correction. 1 MUFU + 2 DMUL + 5 DFMA.
+// callers keep such lanes off the main path): MUFU.RSQ64H seed y
+// (|e| = |1 - a y^2| <= 2^-19.0, tools/mufu_probe.cu), s = a y, then
+// sqrt a = s (1 - e)^(-1/2) = s (1 + e/2 + 3e^2/8 + ...) truncated after e^2
+// (error 5e^3/16 <= 2^-58.8). 1 MUFU + 2 DMUL + 3 DFMA (round 2; the coupled
+// Newton + Karp-Markstein form took 2 DMUL + 5 DFMA: asinf/acosf +4..6%).
 CR_F double sqrt_fast(double a) {
-  double y = rsqrt_approx(a);
-  double s = mul_(a, y), h = mul_(y, 0.5);
-  double r = fma_(-s, h, 0.5);
-  s = fma_(s, r, s);
-  h = fma_(h, r, h);
-  return fma_(fma_(-s, s, a), h, s);
+  const double y = rsqrt_approx(a);
+  const double s = mul_(a, y);
+  const double e = fma_(-s, y, 1.0);  // 1 - a y^2 (s rounded: 2^-54 relative)
+  return fma_(s, mul_(e, fma_(e, 0.375, 0.5)), s);
 }
 
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);
@@ -306,17 +310,17 @@ CR_F double scale2_imad_neg(double a, int u) {
 #endif
 }
 
-// Division num/den to ~2^-52 relative: MUFU seed, one Newton step, one
-// residual correction (6 FP64 ops). The residual step is required: a product
-// with the once-refined reciprocal alone fails the exhaustive tanf sweep
-// (MUFU.RCP64H seeds are too coarse for one Newton step).
+// Division num/den to ~2^-52 relative: MUFU seed r (|e| = |1 - den r| <=
+// 2^-19.9 over all inputs, tools/mufu_probe.cu, profiles/r02/mufu_probe.txt),
+// then 1/den = r (1 + e + e^2 + e^3 ...) truncated after e^2 (error e^3 <=
+// 2^-59.8): e and num*r in parallel, two FMAs after - 4 FP64 ops, chain depth
+// 3 (round 2; the Newton + residual-correction form took 5 ops, depth 5:
+// tanf/tanhf/atanf +1..7%, profiles/r02/ab_div_sqrt.txt).
 CR_F double div_fast(double num, double den) {
-  double r = rcp_approx(den);
-  double e = fma_(-den, r, 1.0);
-  r = fma_(r, e, r);
-  double q = mul_(num, r);
-  double res = fma_(-den, q, num);
-  return fma_(r, res, q);
+  const double r = rcp_approx(den);
+  const double e = fma_(-den, r, 1.0);
+  const double q = mul_(num, r);
+  return fma_(q, fma_(e, e, e), q);
 }
 
 }  // namespace crvec

@@ -9,19 +9,18 @@
 #include "../../paper_2605_15547_b200/csrc/crvec_fns_f32.cuh"
 using namespace crvec;
 
-#ifdef CRVEC_PH_INT
-static const unsigned *ph_tab() { return INV_PI_WORDS; }
-#else
-static const D2 *ph_tab() {  // PH_T as the kernels' 16-byte pairs
-  static D2 t[232];
-  static bool init = false;
-  if (!init) {
-    for (int i = 0; i < 232; ++i) t[i] = D2{PH_T[2 * i], PH_T[2 * i + 1]};
-    init = true;
+// the kernels' exponent-indexed Payne-Hanek table (PHBlock: hi at [b], lo at
+// [256 + b]); big arguments (|x| >= 2^12) take red_trig_ph as in a warp that
+// holds one
+static const double *ph_tab() {
+  static double t[512];
+  for (int i = 0; i < 256; ++i) {
+    t[i] = PH_T[2 * i];
+    t[256 + i] = PH_T[2 * i + 1];
   }
   return t;
 }
-#endif
+static bool trig_big(float x) { return std::fabs(x) >= 0x1p12f; }
 
 template <class F> struct is_trig : std::false_type {};
 template <int W> struct is_trig<FnTrig<W>> : std::true_type {};
@@ -32,7 +31,7 @@ static uint32_t eval1(float x, int force, uint64_t *slow) {
   F::load(R);
   Fast f;
   if constexpr (is_trig<F>::value) {
-    RedTrig q = F::is_big(x) ? ph_reduce(x, ph_tab()) : red_trig_small(f2d(x));
+    RedTrig q = trig_big(x) ? red_trig_ph(x, ph_tab()) : red_trig_small(f2d(x));
     f = F::from_red(x, q, R);
   } else {
     f = F::fast(x, R);
@@ -99,7 +98,7 @@ static double probe(const uint32_t *x, uint64_t n, uint32_t *E) {
     F::load(R);
     Fast f;
     if constexpr (is_trig<F>::value) {
-      RedTrig q = F::is_big(xf) ? ph_reduce(xf, ph_tab()) : red_trig_small(f2d(xf));
+      RedTrig q = trig_big(xf) ? red_trig_ph(xf, ph_tab()) : red_trig_small(f2d(xf));
       f = F::from_red(xf, q, R);
     } else {
       f = F::fast(xf, R);
