@@ -376,7 +376,9 @@ template <> struct KernelShape<FnExp2> { static constexpr int vw = 8, nv = 1, mi
 template <> struct KernelShape<FnExp10> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExp> { static constexpr int vw = 8, nv = 1, minb = 3; };
 template <> struct KernelShape<FnExpm1> { static constexpr int vw = 8, nv = 2, minb = 2; };
-template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 1, minb = 3; };
+// tanh, asin/acos: 8:2:2 after the 4-op division / 5-op sqrt (+1.2..2.7%,
+// profiles/r02/ab_shapes_r2w.txt; the trig kernels lose 3-7% at 8:2:2)
+template <> struct KernelShape<FnTanh> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog1p> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnLog2> { static constexpr int vw = 8, nv = 2, minb = 2; };
@@ -385,7 +387,7 @@ template <> struct KernelShape<FnCosh> { static constexpr int vw = 8, nv = 2, mi
 template <> struct KernelShape<FnLog10> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnAtan> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <> struct KernelShape<FnRsqrt> { static constexpr int vw = 8, nv = 1, minb = 4; };
-template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 8, nv = 1, minb = 3; };
+template <bool A> struct KernelShape<FnAsinAcos<A>> { static constexpr int vw = 8, nv = 2, minb = 2; };
 template <int W> struct KernelShape<FnTrig<W>> { static constexpr int vw = 8, nv = 1, minb = 3; };
 
 // One grid-stride step of the map kernel: issue the loads of the next step
