@@ -281,6 +281,15 @@ CR_F double sqrt_fast(double a) {
   return fma_(s, mul_(e, fma_(e, 0.375, 0.5)), s);
 }
 
+// binary32 -> binary64 for a non-negative NORMAL float by exponent-field
+// arithmetic on the integer pipes (LEA.HI + SHL) instead of F2F on the
+// conversion (XU) pipe; zeros, subnormals, Inf and NaN give garbage, so the
+// callers keep such lanes off the main path (or show the result rounds alike).
+CR_F double f2d_posnorm(uint32_t ub) { return hilo2d((int)((ub >> 3) + (896u << 20)), ub << 29); }
+// ... and back, truncated to binary32 precision (index / comparison use only):
+// the bits of a non-negative normal double as a float, one IMAD.
+CR_F float d2f_trunc(double a) { return u2f((uint32_t)d2hi(a) * 8u + (uint32_t)d2lo(a) / 0x20000000u - (896u << 23)); }
+
 // 2^e scaling of a normal double by exponent-field arithmetic (integer pipe);
 // valid while the result stays normal.
 CR_F double scale2(double a, int e) { return hilo2d(d2hi(a) + (e << 20), d2lo(a)); }

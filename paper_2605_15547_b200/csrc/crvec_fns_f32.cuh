@@ -981,7 +981,7 @@ struct FnAtan {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     float axf = fminf(fabs_(x), 0x1p127f);
-    double z = f2d(axf);
+    double z = f2d_posnorm(f2u(axf));  // exact on the main range (normal |x|)
     bool up = axf > 1.0f;
     const uint32_t kb = f2u(fmaf(up ? rcp_approx_f(axf) : axf, 7.49f, 0x1.8p23f));  // j <= 7
     const SplitRow cs = split_row_kb(R.t, kb, up);
@@ -1034,9 +1034,14 @@ struct FnAsinAcos {
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
     float axf = fminf(fabs_(x), 1.0f);
-    double ax = f2d(axf);
+    // |x| as a double and sqrt(1 - x^2) as a float by exponent-field
+    // arithmetic (integer pipes, not two conversions): exact for the normal
+    // |x| of asin's main range; acos's zero / subnormal lanes get a value
+    // below 2^-126, and acos of that rounds like acos(x) (pi/2 is nowhere near
+    // a binary32 rounding boundary)
+    double ax = f2d_posnorm(f2u(axf));
     double s = sqrt_fast(fma_(-ax, ax, 1.0));  // 1 - x^2 exact
-    float sf = (float)s;
+    float sf = d2f_trunc(s);
     bool up = axf > sf;
     // j = RN(10.5 * min) in the low bits of the 1.5*2^23-shifted sum; (cos,
     // sin, angle) from three columns of one shared row (round 2; round 1 had
