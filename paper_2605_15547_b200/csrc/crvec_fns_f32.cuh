@@ -50,6 +50,7 @@ CR_F const double *sh_split16(const double *A, const double *B, const int *W) {
     tab[i] = A[i];
     if (NC > 1) tab[16 + i] = B[i];
     if (NC > 2) tab[32 + i] = hilo2d(W[i], 0u);
+    if (NC > 3) tab[48 + i] = PI_H - hilo2d(W[i], 0u);  // exact (see FnAsinAcos)
   }
 #if CR_DEVICE
   __syncthreads();
@@ -79,6 +80,16 @@ CR_F SplitRow split_row_kb(const double *t, uint32_t kb, bool up) {
   return {(uint32_t)__cvta_generic_to_shared(t) + (kb * 8u + c)};
 #else
   return {t + ((kb & 7u) + (up ? 8u : 0u))};
+#endif
+}
+// Column at a run-time byte offset (a multiple of 128) of a split row.
+CR_F double split_get_dyn(SplitRow r, uint32_t off) {
+#if CR_DEVICE
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(r.a + off));
+  return v;
+#else
+  return r.p[off / 8];
 #endif
 }
 template <int COL>
@@ -451,7 +462,7 @@ struct FnTanh {
     // reduction of 2|x| with the x2 folded in: k = RN(2|x| 16/ln2), h = r/2 =
     // |x| - k ln2/32 (Cody-Waite on the halved constants, exact first step),
     // (e^r - 1)/2 = h + h^2 2Q(2h); E = T e^r - 1 = 2T (e^r - 1)/2 + (T - 1)
-    const double xd = f2d(fminf(fabs_(x), 10.0f));
+    const double xd = f2d_posnorm(f2u(fminf(fabs_(x), 10.0f)));  // exact on the main range (normal |x|)
     const double t = fma_(xd, INV_LN2_32, SHIFTER);
     const double kd = sub_(t, SHIFTER);
     double h = fma_(kd, -LN2_32_H, xd);  // exact
@@ -1029,7 +1040,8 @@ struct FnAsinAcos {
   CR_F static void load(Regs &R) {
     // (cos, sin, angle) columns: the angle is a third conflict-free LDS.64 off
     // the same row address (one SHFL + a zero-word move before)
-    R.t = ACOS ? sh_split16<102, 3>(ACOS_C, ACOS_S, ACOS_A_HI) : sh_split16<103, 3>(ASIN_C, ASIN_S, ASIN_A_HI);
+    // acos: a fourth column pi_H - angle for x < 0 (acos(-|x|) = pi - acos|x|)
+    R.t = ACOS ? sh_split16<102, 4>(ACOS_C, ACOS_S, ACOS_A_HI) : sh_split16<103, 3>(ASIN_C, ASIN_S, ASIN_A_HI);
   }
   CR_F static Fast fast(float x, const Regs &R) {
     uint32_t xb = f2u(x);
@@ -1048,11 +1060,17 @@ struct FnAsinAcos {
     // the angle in a register table, profiles/r01/ab_shtab_trig.txt)
     const uint32_t kb = f2u(fmaf(up ? sf : axf, 10.5f, 0x1.8p23f));  // j <= 7
     const SplitRow cs = split_row_kb(R.t, kb, up);
-    const double C = split_get<0>(cs), S = split_get<1>(cs), A = split_get<2>(cs);
-    double d = ACOS ? fma_(s, C, -mul_(ax, S)) : fma_(ax, C, -mul_(s, S));
-    double a = add_(A, asinq(d));
-    if (!ACOS) a = with_sign(a, xb);
-    else a = (int)xb < 0 ? add_(PI_H, -a) : a;
+    const double C = split_get<0>(cs), S = split_get<1>(cs);
+    double a;
+    if (!ACOS) {
+      const double d = fma_(ax, C, -mul_(s, S));
+      a = with_sign(add_(split_get<2>(cs), asinq(d)), xb);
+    } else {
+      // x < 0: (pi_H - A) + asin(-d) from the fourth column and a sign flip
+      // of d (one LOP3), instead of pi_H - (A + asin d) (one DADD + selects)
+      const double d = with_sign(fma_(s, C, -mul_(ax, S)), xb);
+      a = add_(split_get_dyn(cs, (int)xb < 0 ? 384u : 256u), asinq(d));
+    }
     return Fast{a, in_main(xb)};
   }
   // asin main: 2^-12 < |x| < 1; acos main: |x| < 1 (s > 0 on the main path)
