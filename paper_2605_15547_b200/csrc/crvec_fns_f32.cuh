@@ -854,9 +854,11 @@ CR_F double flip_k16(double v, int k) { return hilo2d(d2hi(v) ^ ((k << 27) & (in
 template <int WHICH>  // 0: sin, 1: cos, 2: tan
 struct FnTrig {
   static constexpr uint32_t E = WHICH == 2 ? 1024 : 512;
-  // (S_j, C_j): column-split for sin / cos / sincos (+8-10%, conflict-free
-  // LDS.64), interleaved pairs for tan (-2.6% split; profiles/r02/ab_split.txt)
-  static constexpr bool kSplit = WHICH != 2;
+  // (S_j, C_j): column-split (conflict-free LDS.64) for all three. tanf had
+  // interleaved pairs (round 2 r2q: split -2.6%); after its shorter division
+  // the pair LDS.128 conflicts were its top stall and split measured +8.9% on
+  // the config mix, -0.9% uniform (profiles/r02/ab_tan_split_r3a.txt)
+  static constexpr bool kSplit = true;
   struct Regs {
     const double *t;
     const D2 *p;
