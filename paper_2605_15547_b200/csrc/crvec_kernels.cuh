@@ -367,6 +367,11 @@ template <> struct PrefetchL2<FnExpm1> { static constexpr bool value = true; };
 template <int B> struct PrefetchL2<FnLogB<B>> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnLog1p> { static constexpr bool value = true; };
 template <> struct PrefetchL2<FnCosh> { static constexpr bool value = true; };
+// end of round 2: sinh +4.7%, atan / asin / acos +0.5..1% (tanh and trig lose
+// 1-3%; profiles/r02/ab_prefetch_r3b.txt)
+template <> struct PrefetchL2<FnSinh> { static constexpr bool value = true; };
+template <> struct PrefetchL2<FnAtan> { static constexpr bool value = true; };
+template <bool A> struct PrefetchL2<FnAsinAcos<A>> { static constexpr bool value = true; };
 
 template <class F>
 struct KernelShape {
